@@ -1,0 +1,182 @@
+/*
+ * jv.h — C-ABI of the B200-native ILU / stri / spmv library (libjv.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `ilukit` (/root/reference/pkg/src/ilukit).  The reference's own seam is the
+ * L3 -> L0 call from a Python wrapper into a numba kernel that takes flat
+ * int64/float64 arrays plus scalars and mutates outputs in place
+ * (SURVEY.md §1, §8b).  Each entry point below replaces one such kernel (or
+ * a fused group); the replaced reference symbol is cited beside it.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless the name ends in `_h`.
+ *  - Structure arrays are int32 (n, nnz < 2^31; the Python shim checks),
+ *    values are IEEE binary64.
+ *  - Every call is asynchronous on the caller's `stream` (a cudaStream_t
+ *    passed as void*), never synchronises unless documented, and returns
+ *    0 on success or a negative JV_E* code; jv_last_error() describes the
+ *    last failure of the calling thread.
+ *  - Error rows (zero pivot, missing diagonal) are reported through a
+ *    DEVICE int32 slot that the kernels atomicMin into; the caller
+ *    initialises it to INT32_MAX (jv_reset_row) and maps a final value
+ *    < INT32_MAX to ZeroPivotError(row) / MissingDiagonalError(row), exactly
+ *    as the reference raises the smallest bad row after its workers
+ *    quiesce (factor.py:61-63, trisolve.py:54-57, symbolic.py:70-75).
+ *  - Sync-free kernels need a per-plan `epoch` (uint32, strictly increasing
+ *    per call on the same mailbox) so mailboxes never need clearing.
+ */
+#ifndef JV_H
+#define JV_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  JV_OK = 0,
+  JV_EINVAL = -1,     /* bad argument */
+  JV_ECUDA = -2,      /* CUDA runtime error */
+  JV_ENOMEM = -3,     /* workspace too small / allocation failed */
+  JV_ECOOP = -4       /* cooperative launch not possible */
+};
+
+/* ---- context ---------------------------------------------------------- */
+const char* jv_last_error(void);
+int jv_version(void);
+/* number of SMs and the persistent grid each sync-free kernel uses */
+int jv_device_info(int device, int* sms_h, int* coop_h);
+/* *row = INT32_MAX */
+int jv_reset_row(int32_t* row, void* stream);
+
+/* 1 in *hang_h if a sync-free wait gave up because a producer never
+ * published (a schedule bug, never expected); clears it.  Synchronises. */
+int jv_status(int* hang_h);
+
+/* ---- spmv: y = A x ---------------------------------------------------
+ * replaces _kernels.py:28-34 spmv_kernel (called by csr.py:251-260 spmv).
+ * Row sums are accumulated in ascending column order without FMA, so the
+ * result is bitwise equal to the reference for every row of up to
+ * jv_spmv_tile() entries; longer rows use a tree sum (within 1e-12).
+ * tile_rows (nullable) is the jv_spmv_plan output, int32[ntiles+1] with
+ * ntiles = max(1, ceil(nnz / jv_spmv_tile())).                           */
+int jv_spmv_tile(void);
+int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, int32_t* tile_rows,
+                 void* stream);
+int jv_spmv(int32_t n, int32_t nnz, const int32_t* row_start, const int32_t* col,
+            const double* val, const double* x, double* y, const int32_t* tile_rows,
+            void* stream);
+/* Batches of independent systems (config 5) are stored as ONE
+ * block-diagonal CSR (column indices offset by each block's first row), so
+ * every entry point below serves them unchanged and the level schedule of
+ * the block-diagonal matrix interleaves all blocks automatically. */
+
+/* ---- setup (bit-exact structure) ------------------------------------- */
+/* Longest-path depth over the columns < r of each row (forward,
+ * _kernels.py:37-48, whose input is already strictly lower) or the columns
+ * > r swept backward (_kernels.py:51-62).  level_of: int32[n].  ws:
+ * uint64[n] mailbox.
+ * `*nlev_h` receives max level + 1 (this call synchronises the stream). */
+int jv_levels(int backward, int32_t n, const int32_t* row_start, const int32_t* col,
+              int32_t* level_of, uint64_t* ws, uint32_t epoch, int32_t* nlev_h,
+              void* stream);
+/* Stable counting sort by level (= np.argsort(level_of, kind="stable"),
+ * ordering.py:86-94): order[n] and level_ptr[nlev+1] (int32). */
+int jv_level_sort(int32_t n, int32_t nlev, const int32_t* level_of, int32_t* order,
+                  int32_t* level_ptr, void* stream);
+/* Partition rule (ordering.py:119-159) over levels given as level_ptr/order
+ * with integer row nnz; results to host: cut level, n_upper. */
+int jv_partition(int32_t n, int32_t nlev, const int32_t* level_ptr, const int32_t* order,
+                 const int32_t* row_nnz, int32_t min_level_rows, double density_factor,
+                 int suffix_only, int32_t* cut_h, int32_t* n_upper_h, void* stream);
+/* Transpose (csr.py:203-211): out arrays sized n+1/nnz.  t_pos (nullable)
+ * receives, per transposed entry, its source position, so values follow as
+ * t_val[k] = val[t_pos[k]].  Stable: rows ascend within each column. */
+int jv_transpose_pattern(int32_t n, const int32_t* row_start, const int32_t* col,
+                         int32_t* t_row_start, int32_t* t_col, int32_t* t_pos, void* stream);
+/* Pattern of A ∪ Aᵀ then strict lower, fused (csr.py:214-235).  Two-phase:
+ * call with out_col == NULL to get *nnz_h (synchronises), then again. */
+int jv_sym_lower(int32_t n, const int32_t* row_start, const int32_t* col,
+                 const int32_t* t_row_start, const int32_t* t_col, int lower_only,
+                 int32_t* out_row_start, int32_t* out_col, int64_t* nnz_h, void* stream);
+/* B[inv[i], inv[j]] = A[i, j] with sorted rows (csr.py:238-243); val may be
+ * NULL for patterns.  out arrays sized like the input. */
+int jv_permute_symmetric(int32_t n, const int32_t* row_start, const int32_t* col,
+                         const double* val, const int32_t* perm, const int32_t* inv,
+                         int32_t* out_row_start, int32_t* out_col, double* out_val,
+                         void* stream);
+/* First row without a stored diagonal -> *row (atomicMin). symbolic.py:70-75 */
+int jv_check_diagonal(int32_t n, const int32_t* row_start, const int32_t* col,
+                      int32_t* row, void* stream);
+/* ILU(1) fill pattern = A ∪ pattern(strict_lower(A)·strict_upper(A)) with
+ * fill level 0/1 (symbolic.py:86-138 at k = 1).  Two-phase like
+ * jv_sym_lower; out_lev may be NULL. */
+int jv_iluk1_pattern(int32_t n, const int32_t* row_start, const int32_t* col,
+                     int32_t* out_row_start, int32_t* out_col, int32_t* out_lev,
+                     int64_t* nnz_h, void* stream);
+/* Values of the (already permuted) matrix into the factor pattern; fill
+ * positions start at 0; diag_pos found; uncovered entries -> *bad_cover,
+ * missing diagonals -> *bad_diag (both atomicMin rows).  symbolic.py:146-181 */
+int jv_assemble(int32_t n, const int32_t* a_row_start, const int32_t* a_col,
+                const double* a_val, const int32_t* f_row_start, const int32_t* f_col,
+                double* f_val, int32_t* diag_pos, int32_t* bad_cover, int32_t* bad_diag,
+                void* stream);
+/* Row inf-norms of the assembled values, zeros when tau == 0 (factor.py:25) */
+int jv_row_norms(int32_t n, const int32_t* row_start, const double* val, double tau,
+                 double* norms, void* stream);
+/* Host-side RCM (ordering.py:199-266) on a symmetrized int32 pattern (host
+ * arrays).  Setup only; a device version is the next item. */
+int jv_rcm_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h, int32_t* perm_h);
+/* Host-side level-of-fill ILU(k) for k >= 2 (symbolic.py:86-138); outputs
+ * malloc'd (free with jv_free_host); returns nnz or < 0.  k = 1 is device. */
+int64_t jv_iluk_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h, int32_t k,
+                     int32_t** out_row_start_h, int32_t** out_col_h, int32_t** out_lev_h);
+void jv_free_host(void* p);
+
+/* ---- numeric factorization ------------------------------------------
+ * Sync-free up-looking ILU(k,tau) over rows taken in `order` (a
+ * topological order of the factor DAG cut into batches that never hold
+ * two dependent rows: batch_ptr[nbatch+1] indexes order).  Bitwise equal
+ * to factor_serial (_kernels.py:197-204): per-row elimination in ascending
+ * pivot order, no FMA.  Replaces factor_serial_kernel, factor_p2p_kernel,
+ * factor_er_kernel, factor_corner*_kernel and factor_sr_kernel
+ * (_kernels.py:197-343): the upper/lower split changes the schedule, never
+ * the arithmetic.  `mbox`: 16-byte mailbox per stored position (nnz*2
+ * uint64).  `err_row`: min zero-pivot row.                                */
+int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col, double* val,
+              const int32_t* diag_pos, const double* norms, double tau, int milu,
+              const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
+              int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
+              void* stream);
+/* `ready_below`: rows with index < ready_below were factored by an earlier
+ * call (the upper stage before the lower-tail call, lower.py:273-318) and are
+ * read from val directly instead of the mailbox. */
+
+/* ---- triangular solves -----------------------------------------------
+ * forward (which=0): y = L^-1 b, unit L (_kernels.py:348-357);
+ * backward (which=1): x = U^-1 y (_kernels.py:360-366).  Same sync-free
+ * machinery; order/batch_ptr as in jv_factor for the solve's own DAG
+ * (backward: rows of higher index first).  in and out may alias.
+ * `mbox`: 16 bytes per row.  The backward diagonal check
+ * (trisolve.py:54-57) is jv_check_zero_diag.                              */
+int jv_solve(int which, int32_t n, const int32_t* row_start, const int32_t* col,
+             const double* val, const int32_t* diag_pos, const int32_t* order,
+             const int32_t* batch_ptr, int32_t nbatch, const double* in, double* out,
+             uint64_t* mbox, uint32_t epoch, void* stream);
+/* ready_below analogue for solves is not needed: every solve path of the
+ * reference (serial, csrls, ls, ls_lower; trisolve.py:60-182) produces the
+ * same bits, so one sync-free sweep serves all of them. */
+int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,
+                       int32_t* row, void* stream);
+/* schedule builder: cut every level of a level_sort result into batches of
+ * at most 32 rows (one warp; rows of a batch never depend on each other).
+ * batch_ptr sized >= n/32 + nlev + 1; *nbatch_h returned (synchronises). */
+int jv_build_batches(int32_t nlev, const int32_t* level_ptr, int32_t* batch_ptr,
+                     int32_t* nbatch_h, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JV_H */

@@ -1,0 +1,92 @@
+"""ctypes binding of libjv.so, the C-ABI declared in include/jv.h.
+
+The shared library is built in-tree by __graft_entry__.build() (nvcc, sm_100a).
+There is no fallback: if the library or a CUDA device is missing, every
+hot-path call raises BackendUnavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_uint32, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libjv.so")
+
+
+class BackendUnavailable(RuntimeError):
+    """libjv.so or the CUDA device it needs is missing."""
+
+
+_P = c_void_p  # device pointer
+_I32P = POINTER(c_int32)
+
+# name -> argtypes (all return int status unless listed in _RESTYPES)
+_SIGS = {
+    "jv_last_error": [],
+    "jv_version": [],
+    "jv_device_info": [c_int, _I32P, _I32P],
+    "jv_reset_row": [_P, _P],
+    "jv_status": [_I32P],
+    "jv_spmv_tile": [],
+    "jv_spmv_plan": [c_int32, c_int32, _P, _P, _P],
+    "jv_spmv": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P],
+    "jv_levels": [c_int, c_int32, _P, _P, _P, _P, c_uint32, _I32P, _P],
+    "jv_level_sort": [c_int32, c_int32, _P, _P, _P, _P],
+    "jv_partition": [c_int32, c_int32, _P, _P, _P, c_int32, c_double, c_int, _I32P, _I32P, _P],
+    "jv_transpose_pattern": [c_int32, _P, _P, _P, _P, _P, _P],
+    "jv_sym_lower": [c_int32, _P, _P, _P, _P, c_int, _P, _P, POINTER(c_int64), _P],
+    "jv_permute_symmetric": [c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "jv_check_diagonal": [c_int32, _P, _P, _P, _P],
+    "jv_iluk1_pattern": [c_int32, _P, _P, _P, _P, _P, POINTER(c_int64), _P],
+    "jv_assemble": [c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "jv_row_norms": [c_int32, _P, _P, c_double, _P, _P],
+    "jv_rcm_host": [c_int32, _P, _P, _P],
+    "jv_iluk_host": [c_int32, _P, _P, c_int32, POINTER(_I32P), POINTER(_I32P), POINTER(_I32P)],
+    "jv_free_host": [c_void_p],
+    "jv_factor": [c_int32, _P, _P, _P, _P, _P, c_double, c_int, _P, _P, c_int32, c_int32, _P,
+                  c_uint32, _P, _P],
+    "jv_solve": [c_int, c_int32, _P, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, c_uint32, _P],
+    "jv_check_zero_diag": [c_int32, _P, _P, _P, _P],
+    "jv_build_batches": [c_int32, _P, _P, _I32P, _P],
+}
+_RESTYPES = {
+    "jv_last_error": ctypes.c_char_p,
+    "jv_iluk_host": c_int64,
+    "jv_free_host": None,
+}
+
+_lib = None
+
+
+def load():
+    """Load libjv.so once; raise BackendUnavailable if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise BackendUnavailable(
+            f"{LIB_PATH} is not built; run __graft_entry__.build() (nvcc sm_100a)"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, argtypes in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPES.get(name, c_int)
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def call(name, *args):
+    """Invoke a status-returning entry point; raise on a nonzero status."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.jv_last_error().decode(errors="replace")
+        raise RuntimeError(f"{name} failed ({rc}): {msg}")
+    return rc

@@ -1,0 +1,84 @@
+// C-ABI plumbing: error strings, device info, the persistent cooperative
+// launch shared by every sync-free kernel, and the hang detector.
+#include "common.cuh"
+#include "../../include/jv.h"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+namespace jvh {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return JV_ECUDA;
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 1;
+  }
+  return cached[dev];
+}
+
+// Every warp of a sync-free kernel may spin on rows owned by any other warp,
+// so all CTAs must be resident at once: the grid is exactly the occupancy
+// limit and the launch is cooperative (the driver refuses rather than
+// time-slicing a grid that would not fit).
+template <typename K>
+int coop_launch(K kernel, int block, void** args, cudaStream_t stream, const char* what) {
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  if (per_sm < 1) {
+    set_error("%s: kernel cannot be resident", what);
+    return JV_ECOOP;
+  }
+  const int grid = per_sm * sm_count();
+  e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(block), args, 0, stream);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  return JV_OK;
+}
+
+}  // namespace jvh
+
+extern "C" const char* jv_last_error(void) { return jvh::g_err; }
+
+extern "C" int jv_version(void) { return 1; }
+
+extern "C" int jv_device_info(int device, int* sms_h, int* coop_h) {
+  int v = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_device_info");
+  if (sms_h) *sms_h = v;
+  e = cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, device);
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_device_info");
+  if (coop_h) *coop_h = v;
+  return JV_OK;
+}
+
+// 1 if any sync-free wait gave up (a producer never published), then
+// clears the flag.  Synchronises the device.
+extern "C" int jv_status(int* hang_h) {
+  int h = 0, z = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(&h, jv::g_hang, sizeof(int));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_status");
+  if (h) cudaMemcpyToSymbol(jv::g_hang, &z, sizeof(int));
+  if (hang_h) *hang_h = h;
+  return JV_OK;
+}

@@ -1,0 +1,8 @@
+// Single translation unit of libjv.so (one TU keeps the device-side hang
+// flag and the launch helper shared without relocatable device code).
+#include "abi.cu"
+#include "spmv.cu"
+#include "factor.cu"
+#include "solve.cu"
+#include "setup.cu"
+#include "host.cpp"

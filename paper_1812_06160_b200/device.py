@@ -1,0 +1,315 @@
+"""Device-resident objects and the thin Python side of every libjv call.
+
+PyTorch is used only for device memory, the current stream and small
+index plumbing; all arithmetic of the hot path runs in libjv.so kernels.
+Index arrays on the device are int32 (checked), values float64.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import BackendUnavailable
+
+_INT32_MAX = 2**31 - 1
+_NO_ROW = _INT32_MAX
+
+_torch = None
+
+
+def torch():
+    """Import torch lazily and require a CUDA device (no CPU fallback)."""
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    if not _torch.cuda.is_available():
+        raise BackendUnavailable("no CUDA device: the ILU/stri/spmv path runs only on the GPU")
+    _lib.load()
+    return _torch
+
+
+def stream():
+    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def sync():
+    torch().cuda.current_stream().synchronize()
+
+
+def i32(a):
+    """Host index array (any int dtype) -> device int32 tensor."""
+    t = torch()
+    a = np.asarray(a)
+    if a.size and (a.max() > _INT32_MAX or a.min() < -_INT32_MAX):
+        raise OverflowError("index values exceed int32; matrices need n, nnz < 2**31")
+    return t.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to("cuda", non_blocking=False)
+
+
+def f64(a):
+    t = torch()
+    return t.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda")
+
+
+def empty_i32(n):
+    return torch().empty(max(int(n), 1), dtype=torch().int32, device="cuda")
+
+
+def empty_f64(n):
+    return torch().empty(max(int(n), 1), dtype=torch().float64, device="cuda")
+
+
+def host_i64(t, n=None):
+    a = t.cpu().numpy().astype(np.int64)
+    return a if n is None else a[:n]
+
+
+def host_f64(t, n=None):
+    a = t.cpu().numpy().astype(np.float64)
+    return a if n is None else a[:n]
+
+
+class Mailbox:
+    """Sync-free mailbox (16-byte packets or 8-byte words) plus its epoch.
+
+    Epochs grow by one per kernel call, so stale packets from earlier calls
+    never match; on 32-bit wrap the box is zeroed and the epoch restarts.
+    """
+
+    def __init__(self, slots, words_per_slot=2):
+        self.words = words_per_slot
+        self.slots = max(int(slots), 1)
+        self.buf = torch().zeros(self.slots * words_per_slot, dtype=torch().int64, device="cuda")
+        self.epoch = 0
+
+    def next_epoch(self):
+        self.epoch += 1
+        if self.epoch >= 2**32 - 1:
+            self.buf.zero_()
+            self.epoch = 1
+        return self.epoch
+
+    def ensure(self, slots):
+        if slots > self.slots:
+            self.__init__(slots, self.words)
+        return self
+
+
+def reset_row_slot():
+    slot = torch().empty(1, dtype=torch().int32, device="cuda")
+    _lib.call("jv_reset_row", ptr(slot), stream())
+    return slot
+
+
+def read_row_slot(slot):
+    """Host value of an error-row slot; -1 when no row was reported."""
+    v = int(slot.item())
+    return -1 if v == _NO_ROW else v
+
+
+def check_hang():
+    h = ctypes.c_int32(0)
+    _lib.call("jv_status", ctypes.byref(h))
+    if h.value:
+        raise RuntimeError("a sync-free kernel wait timed out (schedule does not cover a dependency)")
+
+
+# ------------------------------------------------------------------ CSR
+
+
+@dataclass
+class DevCsr:
+    """CSR resident in HBM: int32 structure, float64 values (or None)."""
+
+    n: int
+    nnz: int
+    row_start: object
+    col: object
+    val: object = None
+    _tile_rows: object = field(default=None, repr=False)
+
+    @staticmethod
+    def from_host(n, row_start, col, val=None):
+        row_start = np.asarray(row_start)
+        nnz = int(row_start[n]) if n else 0
+        if nnz > _INT32_MAX:
+            raise OverflowError("nnz exceeds int32")
+        return DevCsr(
+            int(n), nnz, i32(row_start), i32(col) if nnz else empty_i32(1),
+            (f64(val) if nnz else empty_f64(1)) if val is not None else None,
+        )
+
+    def tile_rows(self):
+        if self._tile_rows is None:
+            tile = _lib.load().jv_spmv_tile()
+            ntiles = max(1, -(-self.nnz // tile))
+            self._tile_rows = empty_i32(ntiles + 1)
+            _lib.call("jv_spmv_plan", self.n, self.nnz, ptr(self.row_start), ptr(self._tile_rows),
+                      stream())
+        return self._tile_rows
+
+    def host_pattern(self):
+        return host_i64(self.row_start, self.n + 1), host_i64(self.col, self.nnz)
+
+
+def spmv_dev(a: DevCsr, x, y):
+    """y = A x on the device (x, y float64 tensors of length n)."""
+    _lib.call("jv_spmv", a.n, a.nnz, ptr(a.row_start), ptr(a.col), ptr(a.val), ptr(x), ptr(y),
+              ptr(a.tile_rows()), stream())
+    return y
+
+
+# ----------------------------------------------------------- level sets
+
+
+def levels_dev(a: DevCsr, backward: bool):
+    """Longest-path levels (int32 tensor) and the level count."""
+    level_of = empty_i32(a.n)
+    box = Mailbox(a.n, 1)
+    nlev = ctypes.c_int32(0)
+    _lib.call("jv_levels", int(backward), a.n, ptr(a.row_start), ptr(a.col), ptr(level_of),
+              ptr(box.buf), box.next_epoch(), ctypes.byref(nlev), stream())
+    check_hang()
+    return level_of, int(nlev.value)
+
+
+def level_sort_dev(n, nlev, level_of):
+    order = empty_i32(n)
+    level_ptr = empty_i32(nlev + 1)
+    _lib.call("jv_level_sort", n, nlev, ptr(level_of), ptr(order), ptr(level_ptr), stream())
+    return order, level_ptr
+
+
+def batches_dev(nlev, level_ptr, n):
+    batch_ptr = empty_i32(n // 32 + nlev + 2)
+    nb = ctypes.c_int32(0)
+    _lib.call("jv_build_batches", nlev, ptr(level_ptr), ptr(batch_ptr), ctypes.byref(nb), stream())
+    return batch_ptr, int(nb.value)
+
+
+@dataclass
+class Schedule:
+    """Level-batched row order for a sync-free sweep."""
+
+    order: object
+    batch_ptr: object
+    nbatch: int
+    nlev: int
+
+    def restrict(self, lo, hi, level_of):
+        """Rows with lo <= index < hi, keeping the level batching."""
+        t = torch()
+        sel = self.order[(self.order >= lo) & (self.order < hi)].contiguous()
+        if sel.numel() == 0:
+            return Schedule(sel, empty_i32(1), 0, 0)
+        lev = level_of[sel.long()].long()
+        counts = t.bincount(lev, minlength=self.nlev)
+        level_ptr = t.zeros(self.nlev + 1, dtype=t.int64, device="cuda")
+        level_ptr[1:] = t.cumsum(counts, 0)
+        level_ptr = level_ptr.to(t.int32)
+        bp, nb = batches_dev(self.nlev, level_ptr, sel.numel())
+        return Schedule(sel, bp, nb, self.nlev)
+
+
+def schedule_dev(a: DevCsr, backward: bool):
+    level_of, nlev = levels_dev(a, backward)
+    order, level_ptr = level_sort_dev(a.n, nlev, level_of)
+    bp, nb = batches_dev(nlev, level_ptr, a.n)
+    return Schedule(order, bp, nb, nlev), level_of
+
+
+# --------------------------------------------------------- ILU factors
+
+
+class DevIlu:
+    """Factor storage resident in HBM plus the schedules of its three sweeps.
+
+    factor(): sync-free ILU(k, tau) in place on `val`;
+    solve(which, b, out): forward (unit L) / backward (U) sweeps.
+    """
+
+    def __init__(self, n, row_start, col, diag_pos, val=None, tau=0.0, milu=False):
+        self.n = int(n)
+        self.row_start = row_start
+        self.col = col
+        self.diag_pos = diag_pos
+        self.nnz = int(row_start[self.n].item()) if self.n else 0
+        self.val = val if val is not None else empty_f64(self.nnz)
+        self.tau = float(tau)
+        self.milu = bool(milu)
+        self.pattern = DevCsr(self.n, self.nnz, row_start, col)
+        self._fwd = None
+        self._bwd = None
+        self._fwd_levels = None
+        self.norms = empty_f64(self.n)
+        self.fbox = Mailbox(self.nnz, 2)
+        self.sbox = Mailbox(self.n, 2)
+        self.err = reset_row_slot()
+
+    @staticmethod
+    def from_host(n, row_start, col, diag_pos, val, tau=0.0, milu=False):
+        return DevIlu(n, i32(row_start), i32(col) if len(col) else empty_i32(1),
+                      i32(diag_pos) if n else empty_i32(1), f64(val) if len(val) else empty_f64(1),
+                      tau, milu)
+
+    # schedules --------------------------------------------------------
+    def fwd_schedule(self):
+        if self._fwd is None:
+            self._fwd, self._fwd_levels = schedule_dev(self.pattern, False)
+        return self._fwd
+
+    def bwd_schedule(self):
+        if self._bwd is None:
+            self._bwd, _ = schedule_dev(self.pattern, True)
+        return self._bwd
+
+    # numerics ---------------------------------------------------------
+    def compute_norms(self):
+        _lib.call("jv_row_norms", self.n, ptr(self.row_start), ptr(self.val), self.tau,
+                  ptr(self.norms), stream())
+
+    def factor_async(self, lo=0, hi=None, ready_below=0, norms=True):
+        """Launch the factorization of rows [lo, hi) (all by default)."""
+        hi = self.n if hi is None else hi
+        sched = self.fwd_schedule()
+        if lo > 0 or hi < self.n:
+            sched = sched.restrict(lo, hi, self._fwd_levels)
+        if norms:
+            self.compute_norms()
+        _lib.call("jv_reset_row", ptr(self.err), stream())
+        _lib.call("jv_factor", self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
+                  ptr(self.diag_pos), ptr(self.norms), self.tau, int(self.milu), ptr(sched.order),
+                  ptr(sched.batch_ptr), sched.nbatch, int(ready_below), ptr(self.fbox.buf),
+                  self.fbox.next_epoch(), ptr(self.err), stream())
+
+    def factor(self, lo=0, hi=None, ready_below=0):
+        """Factor and return the smallest zero-pivot row (or -1)."""
+        self.factor_async(lo, hi, ready_below)
+        bad = read_row_slot(self.err)
+        check_hang()
+        return bad
+
+    def first_zero_diag(self):
+        slot = reset_row_slot()
+        _lib.call("jv_check_zero_diag", self.n, ptr(self.val), ptr(self.diag_pos), ptr(slot),
+                  stream())
+        return read_row_slot(slot)
+
+    def solve_async(self, which, b, out):
+        sched = self.fwd_schedule() if which == 0 else self.bwd_schedule()
+        _lib.call("jv_solve", which, self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
+                  ptr(self.diag_pos), ptr(sched.order), ptr(sched.batch_ptr), sched.nbatch,
+                  ptr(b), ptr(out), ptr(self.sbox.buf), self.sbox.next_epoch(), stream())
+        return out
+
+    def host_val(self):
+        return host_f64(self.val, self.nnz)
