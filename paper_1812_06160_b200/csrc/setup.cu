@@ -32,10 +32,11 @@ struct Tmp {
 // ---------------------------------------------------------------- levels
 // Longest-path depth, sync-free: row r waits on the level words of its
 // dependencies (columns < r forward, > r backward) and publishes its own.
-// Rows go in index order (ascending forward, descending backward) in
-// batches of 32 per warp; a dependency inside the same warp is resolved by
-// independent thread scheduling (the producer lane always has a smaller
-// distance from the batch start, so some lane can always progress).
+// One warp per row (lanes split the row's dependencies, then a max
+// reduction), rows in index order (ascending forward, descending backward)
+// dealt round-robin to the co-resident warps: a row only waits on rows that
+// precede it in that order, so the lowest unfinished row always progresses,
+// and no lane ever waits on another lane of its own warp.
 struct LevelArgs {
   int n;
   const int32_t* rs;
@@ -48,38 +49,34 @@ struct LevelArgs {
 };
 
 __global__ void __launch_bounds__(256) levels_kernel(LevelArgs A) {
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int T = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int W = (gridDim.x * blockDim.x) >> 5;
   int localmax = -1;
-  for (int k = tid; k < A.n; k += T) {
+  for (int k = gw; k < A.n; k += W) {
     const int r = A.backward ? A.n - 1 - k : k;
     const int a = A.rs[r], b = A.rs[r + 1];
     int m = -1;
-    if (!A.backward) {
-      for (int p = a; p < b; ++p) {
-        const int c = A.col[p];
-        if (c >= r) break;
+    for (int p = a + lane; p < b; p += 32) {
+      const int c = A.col[p];
+      const bool dep = A.backward ? (c > r) : (c < r);
+      if (dep) {
         const int lc = (int)jv::ibox_wait(A.box, c, A.epoch);
         m = lc > m ? lc : m;
       }
-    } else {
-      for (int p = b - 1; p >= a; --p) {
-        const int j = A.col[p];
-        if (j <= r) break;
-        const int lj = (int)jv::ibox_wait(A.box, j, A.epoch);
-        m = lj > m ? lj : m;
-      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const int v = __shfl_xor_sync(0xffffffffu, m, o);
+      m = v > m ? v : m;
     }
     const int lev = m + 1;
-    A.level_of[r] = lev;
-    jv::ibox_put(A.box, r, (uint32_t)lev, A.epoch);
+    if (lane == 0) {
+      A.level_of[r] = lev;
+      jv::ibox_put(A.box, r, (uint32_t)lev, A.epoch);
+    }
     localmax = lev > localmax ? lev : localmax;
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    int v = __shfl_xor_sync(0xffffffffu, localmax, o);
-    localmax = v > localmax ? v : localmax;
-  }
-  if ((threadIdx.x & 31) == 0) atomicMax(A.maxlev, localmax);
+  if (lane == 0 && localmax >= 0) atomicMax(A.maxlev, localmax);
 }
 
 __global__ void iota_kernel(int n, int32_t* out) {

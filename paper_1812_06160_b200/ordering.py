@@ -166,11 +166,14 @@ def partition_stages(
         np.cumsum([len(l) for l in levels], out=level_ptr[1:])
         cut_h = ctypes.c_int32(0)
         nup_h = ctypes.c_int32(0)
+        # keep the device tensors referenced until the call has been issued
+        lp_d = dv.i32(level_ptr)
+        order_d = dv.i32(order)
+        nnz_d = dv.i32(np.asarray(row_nnz, dtype=np.int64))
         _lib.call(
-            "jv_partition", schedule.n, nlev, dv.ptr(dv.i32(level_ptr)), dv.ptr(dv.i32(order)),
-            dv.ptr(dv.i32(np.asarray(row_nnz, dtype=np.int64))), int(config.min_level_rows),
-            float(config.density_factor), int(bool(config.suffix_only)), ctypes.byref(cut_h),
-            ctypes.byref(nup_h), dv.stream(),
+            "jv_partition", schedule.n, nlev, dv.ptr(lp_d), dv.ptr(order_d), dv.ptr(nnz_d),
+            int(config.min_level_rows), float(config.density_factor),
+            int(bool(config.suffix_only)), ctypes.byref(cut_h), ctypes.byref(nup_h), dv.stream(),
         )
         cut = int(cut_h.value)
     else:
