@@ -1,0 +1,417 @@
+"""Benchmark of the ILU / stri / spmv hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl mine|reference]
+
+One step = one pass of the hot path over the config's matrix, inputs
+resident in HBM: refresh the factor values from the assembled matrix,
+numeric factorization (sync-free kernel), forward + backward triangular
+solve, spmv.  `value` is the factorization throughput in factor nonzeros
+per second (BASELINE.json metric "ILU factor nnz/s, stri and spmv GB/s");
+stri and spmv GB/s are reported under "paths".  Every matrix is larger
+than the 126 MB L2, so no flush is needed between steps.
+
+For N > 1 (torchrun, one process per GPU) every rank runs its own replica
+of the single-matrix workload (factorization and stri of one matrix run on
+one GPU: replicas only), `value` aggregates all ranks over the max-over-ranks
+time.  --impl reference times the reference's CPU algorithm (the pinned C
+oracle, threaded point-to-point version) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+HBM_FALLBACK = 6650.0   # GB/s, B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return HBM_FALLBACK, "fallback"
+
+
+def alg_bytes(n, nnz_a, nnz_f):
+    """SURVEY.md §8d algorithmic bytes (int32 indices, fp64 values)."""
+    return dict(
+        spmv=12 * nnz_a + 20 * n + 4,
+        factor=20 * nnz_f + 8 * n + 4,
+        stri=12 * nnz_f + 48 * n + 8,
+    )
+
+
+def build_config(cfg):
+    import paper_1812_06160_b200 as jv
+    from paper_1812_06160_b200 import workloads as W
+    from paper_1812_06160_b200.plan import build_plan
+
+    a, base, s = W.config_matrix(cfg)
+    if base == "rcm":
+        base_perm = jv.rcm_order(a.pattern).perm
+    elif base is None:
+        base_perm = None
+    else:
+        base_perm = base.perm
+    plan = build_plan(a, base_perm=base_perm, k=s["k"], tau=s["tau"],
+                      min_level_rows=s["min_level_rows"])
+    return a, plan, s
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled while the GPU is busy."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, plan, seconds=12.0):
+    """The reference's algorithm on the host (the pinned C oracle), serial
+    and threaded, on the same matrix; bounded to ~`seconds` of CPU work."""
+    import oracle
+    from paper_1812_06160_b200 import device as dv
+
+    ilu = plan.ilu
+    n = ilu.n
+    rs = dv.host_i64(ilu.row_start, n + 1)
+    col = dv.host_i64(ilu.col, ilu.nnz)
+    diag = dv.host_i64(ilu.diag_pos, n)
+    val = dv.host_f64(plan.assembled, ilu.nnz)
+    tau = ilu.tau
+    cores = os.cpu_count() or 1
+    res = {}
+    deadline = time.perf_counter() + seconds
+    ts, tp = [], []
+    while time.perf_counter() < deadline or len(ts) < 2:
+        t0 = time.perf_counter()
+        oracle.factor_serial(rs, col, val, diag, tau)
+        ts.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        oracle.p2p(0, cores, rs, col, val, diag, tau)
+        tp.append(time.perf_counter() - t0)
+        if len(ts) >= 5:
+            break
+    res["serial_s"] = statistics.median(ts)
+    res["threaded_s"] = statistics.median(tp)
+    res["runs"] = len(ts)
+    return res, cores
+
+
+def digest(a, kind):
+    a = np.ascontiguousarray(a, dtype=np.int64 if kind == "i" else np.float64)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def run_mine(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1812_06160_b200 import device as dv
+
+    a, plan, s = build_config(args.config)
+    ilu = plan.ilu
+    n, nnz_f, nnz_a = ilu.n, ilu.nnz, plan.permuted.nnz
+    ab = alg_bytes(n, nnz_a, nnz_f)
+    perm = dv.host_i64(plan.perm, n)
+    b = dv.f64(np.random.default_rng(0).uniform(-1.0, 1.0, n)[perm])
+    y = dv.empty_f64(n)
+    x = dv.empty_f64(n)
+    sy = dv.empty_f64(n)
+    ilu.factor_schedule()
+    ilu.fwd_schedule()
+    ilu.bwd_schedule()
+    plan.permuted.tile_rows()
+
+    def step(ev=None):
+        plan.reset_values()
+        if ev is not None:
+            ev[0].record()
+        ilu.factor_async()
+        if ev is not None:
+            ev[1].record()
+        ilu.solve_async(0, b, y)
+        if ev is not None:
+            ev[2].record()
+        ilu.solve_async(1, y, x)
+        if ev is not None:
+            ev[3].record()
+        dv.spmv_dev(plan.permuted, b, sy)
+        if ev is not None:
+            ev[4].record()
+
+    launches_per_step = 6   # norms, reset_row, factor, fwd, bwd, spmv
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    bad = dv.read_row_slot(ilu.err)
+    dv.check_hang()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    for _ in range(max(args.warmup, 3)):   # keep the GPU busy while the sampler starts
+        step()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0.record()
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = t0.elapsed_time(t1)
+    f_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    fw_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    bw_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    sp_ms = [e[3].elapsed_time(e[4]) for e in evs]
+    times = torch.tensor([total_ms, sum(f_ms), sum(fw_ms) + sum(bw_ms), sum(sp_ms)],
+                         dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    total_ms, f_sum, st_sum, sp_sum = [float(v) for v in times.tolist()]
+    K = args.steps
+    f_avg, st_avg, sp_avg = f_sum / K / 1e3, st_sum / K / 1e3, sp_sum / K / 1e3   # seconds
+
+    # parity of the timed arrays against the reference's full-size digests
+    parity = None
+    dpath = os.path.join(REPO, "tests", "golden", "full_digests.json")
+    if os.path.exists(dpath):
+        d = json.load(open(dpath)).get(args.config)
+        if d:
+            parity = (digest(ilu.host_val(), "f") == d["digests"]["fval"]
+                      and digest(dv.host_f64(x, n), "f") == d["digests"]["x"]
+                      and digest(dv.host_f64(sy, n), "f") == d["digests"]["spmv_perm"])
+
+    # end to end through the public API (host numpy buffers in, out)
+    e2e = measure_e2e(a, plan, args)
+
+    peak, peak_kind = peaks()
+    ach = ab["factor"] / f_avg / 1e9
+    prof = load_profile(args.config)
+    paths = {
+        "factor": {"us": f_avg * 1e6, "nnz_per_s": nnz_f / f_avg, "alg_bytes": ab["factor"],
+                   "GBps": ab["factor"] / f_avg / 1e9, "frac": ab["factor"] / f_avg / 1e9 / peak},
+        "stri": {"us": st_avg * 1e6, "alg_bytes": ab["stri"], "GBps": ab["stri"] / st_avg / 1e9,
+                 "frac": ab["stri"] / st_avg / 1e9 / peak,
+                 "fwd_us": sum(fw_ms) / K * 1e3, "bwd_us": sum(bw_ms) / K * 1e3},
+        "spmv": {"us": sp_avg * 1e6, "alg_bytes": ab["spmv"], "GBps": ab["spmv"] / sp_avg / 1e9,
+                 "frac": ab["spmv"] / sp_avg / 1e9 / peak},
+    }
+    line = {
+        "metric": "ILU factor nnz/s, stri and spmv GB/s (fp64) vs HBM roofline; 1/2/4/8 GPU",
+        "value": world * nnz_f / f_avg,
+        "unit": "factor nnz/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md §8d recipe)",
+        "config": {"workload": f"{args.config}:{s['name']}", "n": n, "nnz_a": nnz_a,
+                   "nnz_f": nnz_f, "k": s["k"], "tau": s["tau"], "levels": plan.nlev,
+                   "n_upper": plan.n_upper, "parallelism": f"replicas{world}",
+                   "l2": "inputs > 126 MB L2, no flush needed"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "peak_kind": peak_kind,
+                     "traffic": prof.get("factor_dram_bytes") if prof else None,
+                     "kernel": "factor_kernel"},
+        "paths": paths,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * K,
+        "clocks": clocks,
+        "parity_vs_reference": parity,
+        "zero_pivot_row": bad,
+    }
+    if world == 1 and rank == 0 and not args.no_cpu:
+        cb, cores = cpu_baseline(args.config, plan, seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": nnz_f / cb["threaded_s"], "unit": "factor nnz/s", "cores": cores,
+            "kind": "port",
+            "sample": f"full {args.config} factorization, threaded p2p oracle x{cb['runs']}",
+            "serial_value": nnz_f / cb["serial_s"], "serial_cores": 1,
+        }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(a, plan, args):
+    """factor_serial through the drop-in API: host values uploaded, factored,
+    downloaded every call (structure and schedules cached on the object)."""
+    import paper_1812_06160_b200 as jv
+    from paper_1812_06160_b200 import device as dv
+    from paper_1812_06160_b200.csr import SparsityPattern
+    from paper_1812_06160_b200.symbolic import IluFactors
+
+    ilu = plan.ilu
+    n = ilu.n
+    pat = SparsityPattern(n, dv.host_i64(ilu.row_start, n + 1), dv.host_i64(ilu.col, ilu.nnz))
+    assembled = dv.host_f64(plan.assembled, ilu.nnz)
+    f = IluFactors(n, pat, assembled.copy(), dv.host_i64(ilu.diag_pos, n),
+                   jv.Permutation(dv.host_i64(plan.perm, n)), ilu.tau, ilu.milu)
+    for _ in range(2):
+        f.val[:] = assembled
+        jv.factor_serial(f)
+    ts = []
+    for _ in range(max(3, min(args.steps, 10))):
+        f.val[:] = assembled
+        t0 = time.perf_counter()
+        jv.factor_serial(f)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"value": ilu.nnz / t, "unit": "factor nnz/s",
+            "h2d_bytes_per_step": 8 * ilu.nnz, "d2h_bytes_per_step": 8 * ilu.nnz,
+            "api": "paper_1812_06160_b200.factor_serial(IluFactors with host numpy values)",
+            "ms": t * 1e3}
+
+
+def load_profile(cfg):
+    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(cfg)
+
+
+def run_reference(args):
+    """The reference's CPU algorithm (pinned C oracle, threaded p2p factor,
+    all host threads) on the same config; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_1812_06160_b200 import workloads as W
+    from oracle import front_end
+
+    a, base, s = W.config_matrix(args.config)
+    if base == "rcm":
+        sym_rs, sym_col = oracle.symmetrize(a.n, a.row_start, a.col)
+        base_perm = oracle.rcm(sym_rs, sym_col)
+    elif base is None:
+        base_perm = None
+    else:
+        base_perm = base.perm
+    fe = front_end(a.n, a.row_start, a.col, a.val, base_perm=base_perm, k=s["k"], tau=s["tau"],
+                   min_level_rows=s["min_level_rows"])
+    rs, col, diag, val = fe["row_start"], fe["col"], fe["diag"], fe["val"]
+    nnz_f = col.size
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.p2p(0, cores, rs, col, val, diag, s["tau"])
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.p2p(0, cores, rs, col, val, diag, s["tau"])
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    v = nnz_f / t
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "ILU factor nnz/s, stri and spmv GB/s (fp64) vs HBM roofline; 1/2/4/8 GPU",
+        "value": v, "unit": "factor nnz/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md §8d recipe)",
+        "config": {"workload": f"{args.config}:{s['name']}", "n": a.n, "nnz_f": nnz_f},
+        "cpu_baseline": {"value": v, "unit": "factor nnz/s", "cores": cores, "kind": "port",
+                         "sample": f"full {args.config} factorization per step, threaded p2p "
+                                   f"restatement of factor_p2p_kernel"},
+        "e2e": {"value": v, "unit": "factor nnz/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mine(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -54,6 +54,16 @@ int jv_reset_row(int32_t* row, void* stream);
 /* 1 in *hang_h if a sync-free wait gave up because a producer never
  * published (a schedule bug, never expected); clears it.  Synchronises. */
 int jv_status(int* hang_h);
+/* probes a single sync-free wait may spend before it gives up and flags
+ * jv_status (default 2^26, ~10 s): a guard against schedule bugs. */
+int jv_set_spin_limit(unsigned limit);
+/* cap (ns) of the exponential __nanosleep backoff of the warp gates that
+ * sync-free kernels use before touching their own mailbox packets
+ * (default 64; 0 = busy poll). */
+int jv_set_backoff(unsigned cap_ns);
+/* diagnostics: record 4 globaltimer stamps per factor batch into buf
+ * (device, 16*batches uint64; NULL disables) */
+int jv_set_trace(unsigned long long* buf, long long batches);
 
 /* ---- spmv: y = A x ---------------------------------------------------
  * replaces _kernels.py:28-34 spmv_kernel (called by csr.py:251-260 spmv).
@@ -144,12 +154,14 @@ void jv_free_host(void* p);
  * factor_er_kernel, factor_corner*_kernel and factor_sr_kernel
  * (_kernels.py:197-343): the upper/lower split changes the schedule, never
  * the arithmetic.  `mbox`: 16-byte mailbox per stored position (nnz*2
- * uint64).  `err_row`: min zero-pivot row.                                */
+ * uint64).  `err_row`: min zero-pivot row.  `ticket`: two int32 words,
+ * zero before the first call; batches are claimed through them in order and
+ * the kernel leaves them zero again.                                      */
 int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col, double* val,
               const int32_t* diag_pos, const double* norms, double tau, int milu,
               const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
               int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
-              void* stream);
+              int32_t* ticket, void* stream);
 /* `ready_below`: rows with index < ready_below were factored by an earlier
  * call (the upper stage before the lower-tail call, lower.py:273-318) and are
  * read from val directly instead of the mailbox. */
@@ -164,7 +176,7 @@ int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col, double* v
 int jv_solve(int which, int32_t n, const int32_t* row_start, const int32_t* col,
              const double* val, const int32_t* diag_pos, const int32_t* order,
              const int32_t* batch_ptr, int32_t nbatch, const double* in, double* out,
-             uint64_t* mbox, uint32_t epoch, void* stream);
+             uint64_t* mbox, uint32_t epoch, int32_t* ticket, void* stream);
 /* ready_below analogue for solves is not needed: every solve path of the
  * reference (serial, csrls, ls, ls_lower; trisolve.py:60-182) produces the
  * same bits, so one sync-free sweep serves all of them. */
@@ -175,6 +187,18 @@ int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,
  * batch_ptr sized >= n/32 + nlev + 1; *nbatch_h returned (synchronises). */
 int jv_build_batches(int32_t nlev, const int32_t* level_ptr, int32_t* batch_ptr,
                      int32_t* nbatch_h, void* stream);
+/* Class-aware schedule used by jv_factor / jv_solve: rows (nullable = 0..m-1)
+ * stably sorted by key = 2*level + class; class-0 rows of a level go 32 to a
+ * batch (thread path), class-1 rows one per batch (warp path).
+ * order[m], batch_ptr sized >= m + nkeys + 1; *nbatch_h (synchronises). */
+int jv_build_schedule(int32_t m, const int32_t* rows, const int32_t* keys, int32_t nkeys,
+                      int32_t* order, int32_t* batch_ptr, int32_t* nbatch_h, void* stream);
+/* row classes: factor (thread path iff <= 8 entries, <= 4 pivots, pivots'
+ * U rows <= 4 entries, no MILU) and solve (thread path iff <= 32 deps) */
+int jv_classify_factor(int32_t n, const int32_t* row_start, const int32_t* col,
+                       const int32_t* diag_pos, int milu, int32_t* cls, void* stream);
+int jv_classify_solve(int which, int32_t n, const int32_t* row_start, const int32_t* diag_pos,
+                      int32_t* cls, void* stream);
 
 #ifdef __cplusplus
 }

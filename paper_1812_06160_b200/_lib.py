@@ -29,6 +29,9 @@ _SIGS = {
     "jv_device_info": [c_int, _I32P, _I32P],
     "jv_reset_row": [_P, _P],
     "jv_status": [_I32P],
+    "jv_set_spin_limit": [ctypes.c_uint],
+    "jv_set_backoff": [ctypes.c_uint],
+    "jv_set_trace": [_P, ctypes.c_longlong],
     "jv_spmv_tile": [],
     "jv_spmv_plan": [c_int32, c_int32, _P, _P, _P],
     "jv_spmv": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P],
@@ -46,10 +49,13 @@ _SIGS = {
     "jv_iluk_host": [c_int32, _P, _P, c_int32, POINTER(_I32P), POINTER(_I32P), POINTER(_I32P)],
     "jv_free_host": [c_void_p],
     "jv_factor": [c_int32, _P, _P, _P, _P, _P, c_double, c_int, _P, _P, c_int32, c_int32, _P,
-                  c_uint32, _P, _P],
-    "jv_solve": [c_int, c_int32, _P, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, c_uint32, _P],
+                  c_uint32, _P, _P, _P],
+    "jv_solve": [c_int, c_int32, _P, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, c_uint32, _P, _P],
     "jv_check_zero_diag": [c_int32, _P, _P, _P, _P],
     "jv_build_batches": [c_int32, _P, _P, _I32P, _P],
+    "jv_build_schedule": [c_int32, _P, _P, c_int32, _P, _P, _I32P, _P],
+    "jv_classify_factor": [c_int32, _P, _P, _P, c_int, _P, _P],
+    "jv_classify_solve": [c_int, c_int32, _P, _P, _P, _P],
 }
 _RESTYPES = {
     "jv_last_error": ctypes.c_char_p,

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 namespace jvh {
 
@@ -41,16 +42,58 @@ int sm_count() {
 // limit and the launch is cooperative (the driver refuses rather than
 // time-slicing a grid that would not fit).
 template <typename K>
-int coop_launch(K kernel, int block, void** args, cudaStream_t stream, const char* what) {
+int coop_launch(K kernel, int block, void** args, cudaStream_t stream, const char* what,
+                size_t smem = 0) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, what);
+  }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
   if (e != cudaSuccess) return cuda_status(e, what);
   if (per_sm < 1) {
     set_error("%s: kernel cannot be resident", what);
     return JV_ECOOP;
   }
+  // JV_BLOCKS_PER_SM caps the resident CTAs per SM (tuning experiments)
+  static int cap = -1;
+  if (cap < 0) {
+    const char* env = getenv("JV_BLOCKS_PER_SM");
+    cap = env ? atoi(env) : 0;
+  }
+  if (cap > 0 && per_sm > cap) per_sm = cap;
   const int grid = per_sm * sm_count();
-  e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(block), args, 0, stream);
+  e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(block), args, smem, stream);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  return JV_OK;
+}
+
+// Persistent grid sized to the occupancy limit, ordinary launch: kernels that
+// take work by ticket never wait on a warp that has not started.
+template <typename K>
+int persistent_launch(K kernel, int block, void** args, cudaStream_t stream, const char* what,
+                      size_t smem = 0) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, what);
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  if (per_sm < 1) {
+    set_error("%s: kernel cannot be resident", what);
+    return JV_ECOOP;
+  }
+  static int cap = -1;
+  if (cap < 0) {
+    const char* env = getenv("JV_BLOCKS_PER_SM");
+    cap = env ? atoi(env) : 0;
+  }
+  if (cap > 0 && per_sm > cap) per_sm = cap;
+  e = cudaLaunchKernel((const void*)kernel, dim3(per_sm * sm_count()), dim3(block), args, smem,
+                       stream);
   if (e != cudaSuccess) return cuda_status(e, what);
   return JV_OK;
 }
@@ -69,6 +112,25 @@ extern "C" int jv_device_info(int device, int* sms_h, int* coop_h) {
   e = cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, device);
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_device_info");
   if (coop_h) *coop_h = v;
+  return JV_OK;
+}
+
+extern "C" int jv_set_trace(unsigned long long* buf, long long batches) {
+  cudaError_t e = cudaMemcpyToSymbol(jv::g_trace, &buf, sizeof(buf));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(jv::g_trace_cap, &batches, sizeof(batches));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_trace");
+  return JV_OK;
+}
+
+extern "C" int jv_set_backoff(unsigned cap_ns) {
+  cudaError_t e = cudaMemcpyToSymbol(jv::g_backoff_cap, &cap_ns, sizeof(unsigned));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_backoff");
+  return JV_OK;
+}
+
+extern "C" int jv_set_spin_limit(unsigned limit) {
+  cudaError_t e = cudaMemcpyToSymbol(jv::g_spin_limit, &limit, sizeof(unsigned));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_spin_limit");
   return JV_OK;
 }
 

@@ -8,25 +8,43 @@
 // is bitwise equal to factor_serial for ANY schedule that respects the
 // dependencies.
 //
-// Schedule: rows come in level batches (<= 32 rows of one level of the
-// factor DAG, so rows of a batch are independent); warp w of a persistent,
-// co-resident (cooperative) grid takes batches w, w+W, ...  Because batch b
-// only depends on batches < b, the lowest unfinished batch can always make
-// progress: no deadlock.  Lane i of the warp owns row order[batch_ptr[b]+i]
-// (thread-per-row: the rows of these configs are short, and one thread per
-// row gives the memory-level parallelism the latency-bound DAG needs).
+// Schedule (jv_build_schedule): rows in level order of the factor DAG; inside
+// a level, "short" rows (<= kR entries, <= kP pivots, <= kU upper entries per
+// pivot, no MILU — every stencil row of configs 1-2) come in batches of 32
+// (lane = row), every other row is a batch of its own (warp = row).  Warp w
+// of a persistent co-resident (cooperative) grid takes batches w, w+W, ...;
+// batch b depends only on batches < b, so the lowest unfinished batch always
+// progresses: deadlock-free.
 //
-// Communication: a finished row publishes its U part (diagonal and upper
-// entries) as mailbox packets (common.cuh); consumers poll the packets of
-// exactly the pivot values they need.  No fences, no flags.
+// Communication: a finished row publishes its U part (diagonal + upper
+// entries) as 16-byte mailbox packets {value, epoch} (common.cuh); consumers
+// probe exactly the packets they need.  A warp first waits at a gate — one
+// lane polls the newest pivot row of the batch with __nanosleep backoff —
+// so the ~10^5 rows resident ahead of the dependency frontier do not flood
+// L2 with probes; then all lanes probe their packets back to back.
+//
+// Thread path: the whole row, its pivots' U rows and the gathered values
+// live in registers (compile-time caps, fully unrolled).  Divisions of
+// pivots whose value no earlier pivot touches are issued together; the
+// dependent chain per hop is then one division plus the per-position
+// update sequence.
+// Warp path: row cached in shared memory, pivots in chunks of 32 (lane k =
+// pivot k: its diagonal position and U range), the matching U entries found
+// by parallel binary searches and compacted into a shared op list, gathered
+// in one parallel probe round, then applied pivot by pivot (lanes over the
+// pivot's updates, which hit distinct positions).
 #include "common.cuh"
 #include "../../include/jv.h"
 
 namespace {
 
-constexpr int kMaxRow = 32;    // thread path: row length cap
-constexpr int kMaxOps = 128;   // thread path: update-op cap
-constexpr int kOut = 0x40;     // op target flag: out-of-pattern (MILU -> diagonal)
+constexpr int kR = 8;       // thread path: row entries
+constexpr int kP = 4;       // thread path: pivots (strict-lower entries)
+constexpr int kU = 4;       // thread path: strict-upper entries per pivot row
+constexpr int kWarpRow = 128;   // warp path: row entries cached in smem
+constexpr int kWarpOps = 256;   // warp path: op list capacity per chunk
+constexpr int kFactorWarps = 8; // warps per CTA
+constexpr int kOut = 1 << 30;   // op target flag: out-of-pattern (MILU -> diagonal)
 
 struct FactorArgs {
   const int32_t* row_start;
@@ -43,206 +61,570 @@ struct FactorArgs {
   uint64_t* mbox;
   uint32_t epoch;
   int32_t* err;
+  int* ticket;
 };
 
-// value of a pivot row's U entry at position q: final in val[] for rows that
-// an earlier call factored, otherwise awaited from the mailbox
+struct WarpArena {
+  double val[kWarpRow];
+  int col[kWarpRow];
+  int opq[kWarpOps];
+  int opw[kWarpOps];
+  double opv[kWarpOps];
+  int opend[32];
+};
+
+// lower_bound of key in arr[lo, hi)
+JV_INLINE int lower_bound(const int32_t* arr, int lo, int hi, int key) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (arr[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// raw probe: issue the load now, check the tag later (no compiler barrier, so
+// consecutive probes are in flight together)
+struct Probe {
+  unsigned long long w0, w1;
+};
+JV_INLINE Probe probe_issue(const uint64_t* box, int64_t slot) {
+  Probe p;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+               : "=l"(p.w0), "=l"(p.w1) : "l"(box + 2 * slot));
+  return p;
+}
+JV_INLINE bool probe_ok(const Probe& p, uint32_t epoch) {
+  return (uint32_t)(p.w0 >> 32) == epoch && (uint32_t)(p.w1 >> 32) == epoch;
+}
+JV_INLINE double probe_val(const Probe& p) {
+  return __longlong_as_double((long long)((p.w0 & 0xffffffffull) | (p.w1 << 32)));
+}
+
+// value of U entry q of pivot row c (final in val[] below ready_below)
 JV_INLINE double pivot_value(const FactorArgs& A, int c, int q) {
   if (c < A.ready_below) return __ldcg(A.val + q);
   return jv::mbox_wait(A.mbox, q, A.epoch);
 }
 
-// lower_bound of key in col[lo, hi)
-JV_INLINE int search_col(const int32_t* col, int lo, int hi, int key) {
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (__ldg(col + mid) < key) lo = mid + 1; else hi = mid;
+// ---------------------------------------------------------------- thread path
+//
+// Per-thread state lives in a shared-memory slice (slot-major, so a warp's
+// accesses to one slot are contiguous): compact loops instead of unrolled
+// register code keep the hot path inside the instruction cache — a fully
+// unrolled first version (64 KB of SASS) spent ~5 us per batch on
+// instruction fetch.
+
+constexpr int kSlotsI = kR + 2 * kP + kP * kU;    // cj | dq | ulen | op list
+constexpr int kSlotsD = kR + kP + kP * kU + kP;   // a | dv | uv | lspec
+constexpr int kThreads = kFactorWarps * 32;
+constexpr size_t kArenaBytes = sizeof(WarpArena) * kFactorWarps;
+
+extern __shared__ __align__(16) unsigned char jv_factor_smem[];
+
+// Per-thread slice of the shared slab: slot-major, one column per thread.
+// Addressed through the kernel's extern __shared__ array so every access
+// compiles to LDS/STS.
+struct Slice {
+  int tid;
+  JV_INLINE int* ib() const {
+    return reinterpret_cast<int*>(jv_factor_smem + kArenaBytes + (size_t)kThreads * kSlotsD * 8);
   }
-  return lo;
-}
-
-// Thread path.  Returns false (without side effects) when the row does not
-// fit the local buffers; the warp then runs the serial path for it.
-__device__ bool factor_row_thread(const FactorArgs& A, int r) {
-  const int rs = __ldg(A.row_start + r), re = __ldg(A.row_start + r + 1);
-  const int len = re - rs;
-  if (len > kMaxRow) return false;
-  const int dloc = __ldg(A.diag + r) - rs;
-  const int nL = dloc;
-
-  int cj[kMaxRow];
-  double a[kMaxRow];
-#pragma unroll 4
-  for (int i = 0; i < len; ++i) {
-    cj[i] = __ldg(A.col + rs + i);
-    a[i] = __ldcs(A.val + rs + i);
+  JV_INLINE double* db() const {
+    return reinterpret_cast<double*>(jv_factor_smem + kArenaBytes);
   }
+  JV_INLINE int& cj(int k) const { return ib()[k * kThreads + tid]; }
+  JV_INLINE int& dq(int k) const { return ib()[(kR + k) * kThreads + tid]; }
+  JV_INLINE int& ul(int k) const { return ib()[(kR + kP + k) * kThreads + tid]; }
+  // update op o: (k << 16) | (t << 8) | target entry
+  JV_INLINE int& op(int o) const { return ib()[(kR + 2 * kP + o) * kThreads + tid]; }
+  JV_INLINE double& a(int k) const { return db()[k * kThreads + tid]; }
+  JV_INLINE double& dv(int k) const { return db()[(kR + k) * kThreads + tid]; }
+  JV_INLINE double& uv(int k, int t) const { return db()[(kR + kP + k * kU + t) * kThreads + tid]; }
+  JV_INLINE double& ls(int k) const { return db()[(kR + kP + kP * kU + k) * kThreads + tid]; }
+};
 
-  // phase 1: structure only (no waiting) — which U entries of which pivot
-  // update which position of this row
-  int dq[kMaxRow];
-  int opend[kMaxRow];
-  int opq[kMaxOps];
-  unsigned char opw[kMaxOps];
-  int nops = 0;
-  for (int k = 0; k < nL; ++k) {
-    const int c = cj[k];
-    const int d = __ldg(A.diag + c);
-    const int ce = __ldg(A.row_start + c + 1);
-    dq[k] = d;
-    const int ulen = ce - d - 1;
-    const int rem = len - k - 1;
-    if (!A.milu && rem > 0 && ulen > 8 * rem) {
-      // long pivot row (hub): search this row's remaining columns in U(c);
-      // the update set is the same, and each target is hit once per pivot
-      for (int w = k + 1; w < len; ++w) {
-        const int q = search_col(A.col, d + 1, ce, cj[w]);
-        if (q < ce && __ldg(A.col + q) == cj[w]) {
-          if (nops == kMaxOps) return false;
-          opq[nops] = q; opw[nops] = (unsigned char)w; ++nops;
-        }
-      }
+struct ShortRow {
+  int rs, len, nL;
+  unsigned miss;      // gather slots still to be awaited (bit k*(kU+1)+u)
+  unsigned opend;     // 5-bit end offset of pivot k's ops at bit 5k
+  double thresh;      // tau * row norm (0 when tau == 0)
+  unsigned touched;   // bit k: a[k] receives an update from an earlier pivot
+  int gate, gate_q;
+};
+
+// structure of a short row (no waiting).  false: caps exceeded.
+JV_INLINE bool short_structure(const FactorArgs& A, int r, ShortRow& R, Slice S) {
+  R.rs = __ldg(A.row_start + r);
+  R.len = __ldg(A.row_start + r + 1) - R.rs;
+  R.nL = __ldg(A.diag + r) - R.rs;
+  R.gate = -1;
+  R.gate_q = 0;
+  R.touched = 0;
+  R.thresh = 0.0;
+  if (R.len > kR || R.nL > kP || A.milu) return false;
+  if (A.tau > 0.0) R.thresh = jv::dmul(A.tau, __ldg(A.norms + r));
+  // every round of loads is issued as one batch (registers), then spilled to
+  // the slice: 4 dependent memory rounds per row instead of one per entry
+  int cj[kR];
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    if (i < R.len) {
+      cj[i] = __ldg(A.col + R.rs + i);
+      S.a(i) = __ldcs(A.val + R.rs + i);
     } else {
-      int w = k + 1;
-      for (int q = d + 1; q < ce; ++q) {
-        const int j = __ldg(A.col + q);
-        while (w < len && cj[w] < j) ++w;
-        if (w < len && cj[w] == j) {
-          if (nops == kMaxOps) return false;
-          opq[nops] = q; opw[nops] = (unsigned char)w; ++nops;
-        } else if (A.milu) {
-          if (nops == kMaxOps) return false;
-          opq[nops] = q; opw[nops] = (unsigned char)(dloc | kOut); ++nops;
-        } else if (w >= len) {
+      cj[i] = -1;
+    }
+  }
+  int dq[kP], ce[kP];
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    S.cj(k) = cj[k];
+    if (k < R.nL) {
+      dq[k] = __ldg(A.diag + cj[k]);
+      ce[k] = __ldg(A.row_start + cj[k] + 1);
+    } else {
+      dq[k] = 0;
+      ce[k] = 1;
+    }
+  }
+#pragma unroll
+  for (int i = kP; i < kR; ++i) S.cj(i) = cj[i];
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    S.dq(k) = dq[k];
+    S.ul(k) = ce[k] - dq[k] - 1;
+    ok &= ce[k] - dq[k] - 1 <= kU;
+  }
+  if (!ok) return false;
+  R.miss = 0;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    if (k < R.nL) {
+      const int ul = ce[k] - dq[k] - 1;
+      if (cj[k] < A.ready_below) {
+        // factored by an earlier call: final in val[]
+        S.dv(k) = __ldcg(A.val + dq[k]);
+#pragma unroll
+        for (int t = 0; t < kU; ++t)
+          if (t < ul) S.uv(k, t) = __ldcg(A.val + dq[k] + 1 + t);
+      } else {
+        R.miss |= ((2u << ul) - 1u) << (k * (kU + 1));
+      }
+    }
+  }
+  if (R.nL > 0) {
+    // pivots ascend: the last one is the newest row
+    const int c = S.cj(R.nL - 1);
+    // the pivot row publishes its U packets in position order: poll the last
+    if (c >= A.ready_below) { R.gate = c; R.gate_q = S.dq(R.nL - 1) + S.ul(R.nL - 1); }
+  }
+  int uc[kP][kU];
+#pragma unroll
+  for (int k = 0; k < kP; ++k)
+#pragma unroll
+    for (int t = 0; t < kU; ++t)
+      uc[k][t] = (t < ce[k] - dq[k] - 1) ? __ldg(A.col + dq[k] + 1 + t) : -1;
+  int nops = 0;
+  R.opend = 0;
+  for (int k = 0; k < R.nL; ++k) {
+    for (int t = 0; t < kU; ++t) {
+      int j = -1;
+#pragma unroll
+      for (int kk = 0; kk < kP; ++kk)
+#pragma unroll
+        for (int tt = 0; tt < kU; ++tt)
+          if (kk == k && tt == t) j = uc[kk][tt];
+      if (j < 0) continue;
+      for (int i = k + 1; i < R.len; ++i) {
+        if (S.cj(i) == j) {
+          S.op(nops++) = (k << 16) | (t << 8) | i;
+          if (i < R.nL) R.touched |= 1u << i;
           break;
         }
       }
     }
-    opend[k] = nops;
+    R.opend |= (unsigned)nops << (5 * k);
   }
-
-  // phase 2: gather the pivot values (waits on the producers)
-  double du[kMaxRow];
-  double ov[kMaxOps];
-  {
-    int o = 0;
-    for (int k = 0; k < nL; ++k) {
-      const int c = cj[k];
-      du[k] = pivot_value(A, c, dq[k]);
-      for (; o < opend[k]; ++o) ov[o] = pivot_value(A, c, opq[o]);
-    }
-  }
-
-  // phase 3: elimination, ascending pivots (reference _kernels.py:172-194)
-  const double thresh = jv::dmul(A.tau, A.norms[r]);
-  int o = 0;
-  for (int k = 0; k < nL; ++k) {
-    const double l = jv::ddiv(a[k], du[k]);
-    if (A.tau > 0.0 && fabs(l) < thresh) {
-      a[k] = 0.0;
-      if (A.milu)
-        for (; o < opend[k]; ++o) a[dloc] = jv::dsub(a[dloc], jv::dmul(l, ov[o]));
-      o = opend[k];
-      continue;
-    }
-    a[k] = l;
-    for (; o < opend[k]; ++o) {
-      const int t = opw[o];
-      const int w = (t & kOut) ? dloc : t;
-      a[w] = jv::dsub(a[w], jv::dmul(l, ov[o]));
-    }
-  }
-
-  // phase 4: publish
-  for (int i = 0; i < len; ++i) __stcg(A.val + rs + i, a[i]);
-  for (int i = nL; i < len; ++i) jv::mbox_put(A.mbox, rs + i, a[i], A.epoch);
-  if (a[dloc] == 0.0) atomicMin(A.err, r);
   return true;
 }
 
-// Serial path for long rows: the reference algorithm in place on val[],
-// pivot values from the mailbox.  Run by one lane.
-__device__ void factor_row_serial(const FactorArgs& A, int r) {
-  const int rs = A.row_start[r], re = A.row_start[r + 1];
-  const int dpos = A.diag[r];
-  double* val = A.val;
-  const double thresh = jv::dmul(A.tau, A.norms[r]);
-  for (int p = rs; p < re; ++p) {
-    const int c = A.col[p];
-    if (c >= r) break;
-    const int d = A.diag[c], ce = A.row_start[c + 1];
-    const double l = jv::ddiv(val[p], pivot_value(A, c, d));
-    if (A.tau > 0.0 && fabs(l) < thresh) {
-      val[p] = 0.0;
-      if (A.milu)
-        for (int q = d + 1; q < ce; ++q)
-          val[dpos] = jv::dsub(val[dpos], jv::dmul(l, pivot_value(A, c, q)));
-      continue;
-    }
-    val[p] = l;
-    const int ulen = ce - d - 1, rem = re - p - 1;
-    if (!A.milu && rem > 0 && ulen > 8 * rem) {
-      for (int w = p + 1; w < re; ++w) {
-        const int q = search_col(A.col, d + 1, ce, A.col[w]);
-        if (q < ce && A.col[q] == A.col[w])
-          val[w] = jv::dsub(val[w], jv::dmul(l, pivot_value(A, c, q)));
+// Gather of a short row's pivot values.  The wait is warp-converged: every
+// lane re-probes only its still-missing packets, then the warp votes; lanes
+// never spin on their own (divergent per-lane spin loops inside one warp
+// were measured to stretch a hop to ~20 us on config 2).
+JV_INLINE void short_gather(const FactorArgs& A, const ShortRow& R, Slice S, unsigned mask) {
+  constexpr int kSlots = kP * (kU + 1);
+  // slot (k, u): u = 0 the pivot's diagonal, u > 0 its u-th upper entry;
+  // R.miss was prepared before the gate (pivots factored by an earlier call
+  // were read there already)
+  unsigned miss = R.miss;
+  int dq[kP];
+#pragma unroll
+  for (int k = 0; k < kP; ++k) dq[k] = S.dq(k);
+  unsigned ns = 0, spins = 0;
+  while (__any_sync(mask, miss)) {
+    Probe p[kSlots];
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl)
+      if (miss & (1u << sl)) p[sl] = probe_issue(A.mbox, dq[sl / (kU + 1)] + sl % (kU + 1));
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      if ((miss & (1u << sl)) && probe_ok(p[sl], A.epoch)) {
+        const int k = sl / (kU + 1), u = sl % (kU + 1);
+        if (u == 0) S.dv(k) = probe_val(p[sl]); else S.uv(k, u - 1) = probe_val(p[sl]);
+        miss &= ~(1u << sl);
       }
-      continue;
     }
-    int w = p + 1;
-    for (int q = d + 1; q < ce; ++q) {
-      const int j = A.col[q];
-      while (w < re && A.col[w] < j) ++w;
-      if (w < re && A.col[w] == j)
-        val[w] = jv::dsub(val[w], jv::dmul(l, pivot_value(A, c, q)));
-      else if (A.milu)
-        val[dpos] = jv::dsub(val[dpos], jv::dmul(l, pivot_value(A, c, q)));
-      else if (w >= re)
+    if (__any_sync(mask, miss)) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(2 * ns, 128u) : 16u;
+      if (++spins == jv::g_spin_limit) {
+        atomicExch(&jv::g_hang, 1);
         break;
+      }
     }
   }
-  for (int p = dpos; p < re; ++p) jv::mbox_put(A.mbox, p, val[p], A.epoch);
-  if (val[dpos] == 0.0) atomicMin(A.err, r);
 }
 
-__global__ void __launch_bounds__(256) factor_kernel(FactorArgs A) {
+JV_INLINE void short_finish(const FactorArgs& A, int r, const ShortRow& R, Slice S,
+                            unsigned mask, int cur_batch) {
+  short_gather(A, R, S, mask);
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) jv::trace_mark(cur_batch, 7);
+  // divisions of untouched pivots: independent, issued together
+  double ls[kP];
+#pragma unroll
+  for (int k = 0; k < kP; ++k) ls[k] = (k < R.nL) ? jv::ddiv(S.a(k), S.dv(k)) : 0.0;
+  const double thresh = R.thresh;
+  int o = 0;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    if (k < R.nL) {
+      const double l = (R.touched & (1u << k)) ? jv::ddiv(S.a(k), S.dv(k)) : ls[k];
+      const bool drop = A.tau > 0.0 && fabs(l) < thresh;
+      S.a(k) = drop ? 0.0 : l;
+      const int oe = (R.opend >> (5 * k)) & 31;
+      if (!drop) {
+        for (; o < oe; ++o) {
+          const int op = S.op(o);
+          const int w = op & 0xff, t = (op >> 8) & 0xff;
+          S.a(w) = jv::dsub(S.a(w), jv::dmul(l, S.uv(k, t)));
+        }
+      }
+      o = oe;
+    }
+  }
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) jv::trace_mark2(cur_batch);
+  for (int i = 0; i < R.len; ++i) {
+    const double v = S.a(i);
+    __stcg(A.val + R.rs + i, v);
+    if (i >= R.nL) jv::mbox_put(A.mbox, R.rs + i, v, A.epoch);
+  }
+  if (S.a(R.nL) == 0.0) atomicMin(A.err, r);
+}
+
+// ------------------------------------------------------------------ warp path
+
+// Apply all pivots of row r with the whole warp.
+JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
+  const unsigned full = 0xffffffffu;
+  const int rs = A.row_start[r], re = A.row_start[r + 1];
+  const int len = re - rs;
+  const int dloc = A.diag[r] - rs;
+  const int nL = dloc;
+  const bool cached = len <= kWarpRow;
+  double* av = cached ? W.val : A.val + rs;
+  const int* ac = cached ? W.col : A.col + rs;
+  if (cached) {
+    for (int i = lane; i < len; i += 32) {
+      W.col[i] = A.col[rs + i];
+      W.val[i] = __ldcs(A.val + rs + i);
+    }
+    __syncwarp();
+  }
+  const double thresh = jv::dmul(A.tau, A.norms[r]);
+
+  for (int k0 = 0; k0 < nL;) {
+    const int kc = min(32, nL - k0);
+    int c = -1, d = 0, ce = 0;
+    if (lane < kc) {
+      c = ac[k0 + lane];
+      d = A.diag[c];
+      ce = A.row_start[c + 1];
+    }
+    // ---- structure of the chunk: op list (q, target) per pivot
+    int nops = 0, kdone = 0;
+    bool direct = false;
+    for (int kk = 0; kk < kc; ++kk) {
+      const int k = k0 + kk;
+      const int dk = __shfl_sync(full, d, kk), cek = __shfl_sync(full, ce, kk);
+      const int ulen = cek - dk - 1, rem = len - k - 1;
+      const int cand = A.milu ? ulen : min(ulen, rem);
+      if (nops + cand > kWarpOps) {
+        if (kk == 0) direct = true;   // a single pivot larger than the list
+        break;
+      }
+      if (A.milu) {
+        for (int base = dk + 1; base < cek; base += 32) {
+          const int q = base + lane;
+          int w = -1;
+          if (q < cek) {
+            const int j = A.col[q];
+            const int p = lower_bound(ac, k + 1, len, j);
+            w = (p < len && ac[p] == j) ? p : (dloc | kOut);
+          }
+          const unsigned m = __ballot_sync(full, w >= 0);
+          if (w >= 0) {
+            const int pos = nops + __popc(m & ((1u << lane) - 1));
+            W.opq[pos] = q;
+            W.opw[pos] = w;
+          }
+          nops += __popc(m);
+        }
+      } else if (ulen > rem) {
+        for (int base = k + 1; base < len; base += 32) {
+          const int w = base + lane;
+          int q = -1;
+          if (w < len) {
+            const int p = lower_bound(A.col, dk + 1, cek, ac[w]);
+            if (p < cek && A.col[p] == ac[w]) q = p;
+          }
+          const unsigned m = __ballot_sync(full, q >= 0);
+          if (q >= 0) {
+            const int pos = nops + __popc(m & ((1u << lane) - 1));
+            W.opq[pos] = q;
+            W.opw[pos] = w;
+          }
+          nops += __popc(m);
+        }
+      } else {
+        for (int base = dk + 1; base < cek; base += 32) {
+          const int q = base + lane;
+          int w = -1;
+          if (q < cek) {
+            const int j = A.col[q];
+            const int p = lower_bound(ac, k + 1, len, j);
+            if (p < len && ac[p] == j) w = p;
+          }
+          const unsigned m = __ballot_sync(full, w >= 0);
+          if (w >= 0) {
+            const int pos = nops + __popc(m & ((1u << lane) - 1));
+            W.opq[pos] = q;
+            W.opw[pos] = w;
+          }
+          nops += __popc(m);
+        }
+      }
+      if (lane == 0) W.opend[kk] = nops;
+      kdone = kk + 1;
+    }
+    __syncwarp();
+
+    if (direct) {
+      // one pivot whose updates exceed the op list: wait and apply in place
+      const int k = k0;
+      const int dk = __shfl_sync(full, d, 0), cek = __shfl_sync(full, ce, 0);
+      const int ck = __shfl_sync(full, c, 0);
+      double l = 0.0;
+      int drop = 0;
+      if (lane == 0) {
+        l = jv::ddiv(av[k], pivot_value(A, ck, dk));
+        drop = A.tau > 0.0 && fabs(l) < thresh;
+        av[k] = drop ? 0.0 : l;
+      }
+      l = __shfl_sync(full, l, 0);
+      drop = __shfl_sync(full, drop, 0);
+      __syncwarp();
+      const int ulen = cek - dk - 1, rem = len - k - 1;
+      if (A.milu) {
+        if (lane == 0) {
+          int w = k + 1;
+          for (int q = dk + 1; q < cek; ++q) {
+            const double u = pivot_value(A, ck, q);
+            if (drop) { av[dloc] = jv::dsub(av[dloc], jv::dmul(l, u)); continue; }
+            const int j = A.col[q];
+            while (w < len && ac[w] < j) ++w;
+            const int t = (w < len && ac[w] == j) ? w : dloc;
+            av[t] = jv::dsub(av[t], jv::dmul(l, u));
+          }
+        }
+      } else if (!drop) {
+        if (ulen > rem) {
+          for (int w = k + 1 + lane; w < len; w += 32) {
+            const int p = lower_bound(A.col, dk + 1, cek, ac[w]);
+            if (p < cek && A.col[p] == ac[w])
+              av[w] = jv::dsub(av[w], jv::dmul(l, pivot_value(A, ck, p)));
+          }
+        } else {
+          for (int q = dk + 1 + lane; q < cek; q += 32) {
+            const int j = A.col[q];
+            const int p = lower_bound(ac, k + 1, len, j);
+            if (p < len && ac[p] == j) av[p] = jv::dsub(av[p], jv::dmul(l, pivot_value(A, ck, q)));
+          }
+        }
+      }
+      __syncwarp();
+      k0 += 1;
+      continue;
+    }
+
+    // ---- gate on the newest pivot of the chunk, then gather
+    int g = (lane < kdone && c >= A.ready_below) ? c : -1, gq = d;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int og = __shfl_xor_sync(full, g, o), oq = __shfl_xor_sync(full, gq, o);
+      if (og > g) { g = og; gq = oq; }
+    }
+    if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, gq, A.epoch);
+    __syncwarp();
+    double dv = 1.0;
+    if (lane < kdone) dv = pivot_value(A, c, d);
+    for (int kk = 0, o0 = 0; kk < kdone; ++kk) {
+      const int ck = __shfl_sync(full, c, kk);
+      const int o1 = W.opend[kk];
+      for (int o = o0 + lane; o < o1; o += 32) W.opv[o] = pivot_value(A, ck, W.opq[o]);
+      o0 = o1;
+    }
+    __syncwarp();
+
+    // ---- elimination, pivot by pivot
+    for (int kk = 0, o0 = 0; kk < kdone; ++kk) {
+      const int k = k0 + kk;
+      const int o1 = W.opend[kk];
+      const double dk = __shfl_sync(full, dv, kk);
+      double l = 0.0;
+      int drop = 0;
+      if (lane == 0) {
+        l = jv::ddiv(av[k], dk);
+        drop = A.tau > 0.0 && fabs(l) < thresh;
+        av[k] = drop ? 0.0 : l;
+      }
+      l = __shfl_sync(full, l, 0);
+      drop = __shfl_sync(full, drop, 0);
+      if (A.milu) {
+        // the diagonal accumulates in q order: one lane
+        if (lane == 0)
+          for (int o = o0; o < o1; ++o) {
+            const int t = (drop || (W.opw[o] & kOut)) ? dloc : W.opw[o];
+            av[t] = jv::dsub(av[t], jv::dmul(l, W.opv[o]));
+          }
+      } else if (!drop) {
+        for (int o = o0 + lane; o < o1; o += 32) {
+          const int t = W.opw[o];
+          av[t] = jv::dsub(av[t], jv::dmul(l, W.opv[o]));
+        }
+      }
+      o0 = o1;
+      __syncwarp();
+    }
+    k0 += kdone;
+  }
+
+  // ---- publish
+  for (int i = lane; i < len; i += 32) {
+    const double v = av[i];
+    if (cached) __stcg(A.val + rs + i, v);
+    if (i >= nL) jv::mbox_put(A.mbox, rs + i, v, A.epoch);
+  }
+  if (lane == 0 && av[dloc] == 0.0) atomicMin(A.err, r);
+  __syncwarp();
+}
+
+constexpr size_t kFactorSmem =
+    sizeof(WarpArena) * kFactorWarps + (size_t)kThreads * (kSlotsI * 4 + kSlotsD * 8);
+
+__global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
+  WarpArena* arena = reinterpret_cast<WarpArena*>(jv_factor_smem);
+  const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  for (int b = gw; b < A.nbatch; b += W) {
+  WarpArena& W = arena[threadIdx.x >> 5];
+  const Slice S{(int)threadIdx.x};
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (;;) {
+    const int b = jv::ticket_next(A.ticket, lane);
+    if (b >= A.nbatch) break;
     const int lo = A.batch_ptr[b], hi = A.batch_ptr[b + 1];
     const int idx = lo + lane;
     const bool active = idx < hi;
     const int r = active ? A.order[idx] : -1;
-    bool done = true;
-    if (active) done = factor_row_thread(A, r);
-    unsigned pend = __ballot_sync(0xffffffffu, !done);
+    if (lane == 0) jv::trace_mark(b, 1);
+    ShortRow R;
+    bool fits = false;
+    if (active) fits = short_structure(A, r, R, S);
+    __syncwarp();
+    if (lane == 0) jv::trace_mark(b, 2);
+    // warp gate on the newest pivot of the batch's short rows
+    int g = fits ? R.gate : -1, gq = fits ? R.gate_q : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int og = __shfl_xor_sync(full, g, o), oq = __shfl_xor_sync(full, gq, o);
+      if (og > g) { g = og; gq = oq; }
+    }
+    if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, gq, A.epoch);
+    __syncwarp();
+    if (lane == 0) jv::trace_mark(b, 3);
+    const unsigned fmask = __ballot_sync(full, fits);
+    if (fits) short_finish(A, r, R, S, fmask, b);
+    unsigned pend = __ballot_sync(full, active && !fits);
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
-      const int rr = __shfl_sync(0xffffffffu, r, src);
-      if (lane == 0) factor_row_serial(A, rr);
-      __syncwarp();
+      warp_row(A, __shfl_sync(full, r, src), lane, W);
+    }
+    __syncwarp();
+    if (lane == 0) jv::trace_mark(b, 4);
+  }
+  jv::ticket_exit(A.ticket, lane, nw);
+}
+
+// row classes for the schedule: 0 = thread path, 1 = warp path
+__global__ void classify_factor_kernel(int n, const int32_t* rs, const int32_t* diag, int milu,
+                                       int32_t* cls) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int len = rs[r + 1] - rs[r];
+    const int nL = diag[r] - rs[r];
+    cls[r] = (!milu && len <= kR && nL <= kP) ? 0 : 1;
+  }
+}
+
+__global__ void classify_factor_pivots_kernel(int n, const int32_t* rs, const int32_t* col,
+                                              const int32_t* diag, int32_t* cls) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (cls[r]) continue;
+    const int nL = diag[r] - rs[r];
+    for (int k = 0; k < nL; ++k) {
+      const int c = col[rs[r] + k];
+      if (rs[c + 1] - diag[c] - 1 > kU) { cls[r] = 1; break; }
     }
   }
 }
 
 }  // namespace
 
-
-
 extern "C" int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col, double* val,
                          const int32_t* diag_pos, const double* norms, double tau, int milu,
                          const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
                          int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
-                         void* stream) {
+                         int32_t* ticket, void* stream) {
   if (n < 0 || nbatch < 0 || epoch == 0) {
     jvh::set_error("jv_factor: bad argument (n=%d nbatch=%d epoch=%u)", n, nbatch, epoch);
     return JV_EINVAL;
   }
   if (n == 0 || nbatch == 0) return JV_OK;
   FactorArgs A{row_start, col, val, diag_pos, norms, tau, milu, order, batch_ptr,
-               nbatch, ready_below, mbox, epoch, err_row};
+               nbatch, ready_below, mbox, epoch, err_row, ticket};
   void* args[] = {&A};
-  return jvh::coop_launch(factor_kernel, 256, args, (cudaStream_t)stream, "jv_factor");
+  return jvh::persistent_launch(factor_kernel, kThreads, args, (cudaStream_t)stream, "jv_factor",
+                                kFactorSmem);
+}
+
+extern "C" int jv_classify_factor(int32_t n, const int32_t* row_start, const int32_t* col,
+                                  const int32_t* diag_pos, int milu, int32_t* cls, void* stream) {
+  if (n <= 0) return JV_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = (n + 255) / 256;
+  classify_factor_kernel<<<grid, 256, 0, s>>>(n, row_start, diag_pos, milu, cls);
+  classify_factor_pivots_kernel<<<grid, 256, 0, s>>>(n, row_start, col, diag_pos, cls);
+  JV_CHECK_LAUNCH("jv_classify_factor");
+  return JV_OK;
 }

@@ -164,6 +164,25 @@ __global__ void batch_fill_kernel(int nlev, const int32_t* level_ptr, const int3
   }
 }
 
+// class-aware schedule: groups = (level, class) in key order (key = 2*level
+// + class); class 0 rows are cut into batches of 32, class 1 rows one each
+__global__ void group_batch_count_kernel(int ngroups, const int32_t* gptr, int32_t* cnt) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+    const int c = gptr[g + 1] - gptr[g];
+    cnt[g] = (g & 1) ? c : (c + 31) / 32;
+  }
+}
+__global__ void group_batch_fill_kernel(int ngroups, const int32_t* gptr, const int32_t* boff,
+                                        int32_t* batch_ptr, int m) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+    const int a = gptr[g], b = gptr[g + 1];
+    const int step = (g & 1) ? 1 : 32;
+    int o = boff[g];
+    for (int s = a; s < b; s += step) batch_ptr[o++] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) batch_ptr[boff[ngroups]] = m;
+}
+
 // ------------------------------------------------------- pattern helpers
 __global__ void row_ids_kernel(int n, const int32_t* rs, int32_t* rows) {
   // one warp per row writes its id over the row's nonzeros
@@ -678,5 +697,53 @@ extern "C" int jv_row_norms(int32_t n, const int32_t* row_start, const double* v
   row_norms_kernel<<<grid_for(n), kSetupThreads, 0, (cudaStream_t)stream>>>(n, row_start, val, tau,
                                                                             norms);
   JV_CHECK_LAUNCH("jv_row_norms");
+  return JV_OK;
+}
+
+extern "C" int jv_build_schedule(int32_t m, const int32_t* rows, const int32_t* keys, int32_t nkeys,
+                                 int32_t* order, int32_t* batch_ptr, int32_t* nbatch_h,
+                                 void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m < 0 || nkeys < 0) { jvh::set_error("jv_build_schedule: bad argument"); return JV_EINVAL; }
+  if (m == 0) {
+    set_int_kernel<<<1, 1, 0, s>>>(batch_ptr, 0);
+    *nbatch_h = 0;
+    return JV_OK;
+  }
+  int bits = 1;
+  while ((1LL << bits) < (long long)nkeys) ++bits;
+  Tmp iota(s), skeys(s), tmp(s), gptr(s), cnt(s), off(s);
+  if (!rows) {
+    CK_CUDA(iota.alloc(sizeof(int32_t) * m), "alloc");
+    iota_kernel<<<grid_for(m), kSetupThreads, 0, s>>>(m, (int32_t*)iota.p);
+    rows = (const int32_t*)iota.p;
+  }
+  CK_CUDA(skeys.alloc(sizeof(int32_t) * m), "alloc");
+  size_t tb = 0, tb2 = 0;
+  CK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, (int32_t*)skeys.p, rows, order, m, 0,
+                                          bits, s), "sort size");
+  CK_CUDA(cnt.alloc(sizeof(int32_t) * (nkeys + 1)), "alloc");
+  CK_CUDA(off.alloc(sizeof(int32_t) * (nkeys + 1)), "alloc");
+  CK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, (int32_t*)cnt.p, (int32_t*)off.p, nkeys + 1, s),
+          "scan size");
+  CK_CUDA(tmp.alloc(tb > tb2 ? tb : tb2), "alloc");
+  CK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, (int32_t*)skeys.p, rows, order, m, 0,
+                                          bits, s), "sort");
+  CK_CUDA(gptr.alloc(sizeof(int32_t) * (nkeys + 1)), "alloc");
+  level_ptr_kernel<<<grid_for(m), kSetupThreads, 0, s>>>(m, nkeys, (const int32_t*)skeys.p,
+                                                         (int32_t*)gptr.p);
+  group_batch_count_kernel<<<grid_for(nkeys), kSetupThreads, 0, s>>>(nkeys, (const int32_t*)gptr.p,
+                                                                     (int32_t*)cnt.p);
+  set_int_kernel<<<1, 1, 0, s>>>((int32_t*)cnt.p + nkeys, 0);
+  CK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, (int32_t*)cnt.p, (int32_t*)off.p, nkeys + 1, s),
+          "scan");
+  group_batch_fill_kernel<<<grid_for(nkeys), kSetupThreads, 0, s>>>(
+      nkeys, (const int32_t*)gptr.p, (const int32_t*)off.p, batch_ptr, m);
+  JV_CHECK_LAUNCH("jv_build_schedule");
+  int32_t nb = 0;
+  CK_CUDA(cudaMemcpyAsync(&nb, (int32_t*)off.p + nkeys, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+          "copy");
+  CK_CUDA(cudaStreamSynchronize(s), "sync");
+  *nbatch_h = nb;
   return JV_OK;
 }

@@ -5,17 +5,26 @@
 //            subtraction chain in ascending column order;
 //   backward (_kernels.py:360-366): x[r] = (y[r] - sum_{c>r} u_rc x[c]) / u_rr.
 // Every reference solve path (serial, CSR-LS, p2p, two-stage;
-// trisolve.py:60-182) yields the same bits, and so does this kernel: one row
-// per thread, the row's chain evaluated in the reference order with
-// explicitly rounded ops, dependencies awaited through mailbox packets
-// (common.cuh).  Rows come in level batches of the solve's own DAG (forward:
-// levels of lower(F); backward: reversed levels of upper(F)); warp w of a
-// co-resident grid takes batches w, w+W, ... (deadlock-free: batch b only
-// waits on batches < b).
+// trisolve.py:60-182) yields the same bits, and so does this kernel: each
+// row's chain is evaluated in the reference order with explicitly rounded
+// ops, dependencies awaited through mailbox packets (common.cuh).
+//
+// Schedule (jv_build_schedule): rows in level order of the solve's own DAG
+// (forward: levels of lower(F); backward: reversed levels of upper(F)); rows
+// with <= kThreadDeps dependencies come 32 to a batch (lane = row), longer
+// rows (R-MAT hubs) one to a batch (warp = row: lanes gather 32 dependencies
+// at a time, products formed in parallel, the subtraction chain kept in
+// order by one lane).  Warp w of a co-resident grid takes batches w, w+W,
+// ... (deadlock-free: batch b only waits on batches < b).  Each warp first
+// waits at a gate (one lane, __nanosleep backoff) on the batch's newest
+// dependency.
 #include "common.cuh"
 #include "../../include/jv.h"
 
 namespace {
+
+constexpr int kThreadDeps = 32;   // longer rows take the warp path
+constexpr int kProbe = 8;         // dependency values probed together per round
 
 struct SolveArgs {
   const int32_t* row_start;
@@ -29,72 +38,137 @@ struct SolveArgs {
   double* out;
   uint64_t* mbox;
   uint32_t epoch;
+  int* ticket;
 };
 
-constexpr int kProbe = 8;   // dependency values probed together per round
-
-// Wait for the values of columns col[p0..p1) and fold them into s in
-// ascending order: s -= val[p] * v[c].  The probes of a group of kProbe
-// dependencies are issued back to back so their L2 round trips overlap;
-// only not-yet-published ones are re-polled.
-JV_INLINE double fold_deps(const SolveArgs& A, int p0, int p1, double s) {
-  for (int g = p0; g < p1; g += kProbe) {
-    const int m = min(kProbe, p1 - g);
-    double v[kProbe];
-    int c[kProbe];
-    unsigned ready = 0;
+// Converged wait: every lane re-probes its missing slots, the warp votes,
+// nobody spins alone (divergent per-lane spin loops resolve slowly).
+template <int N>
+JV_INLINE void gather_conv(const SolveArgs& A, const int (&c)[N], double (&v)[N], unsigned miss,
+                           unsigned mask) {
+  unsigned ns = 0, spins = 0;
+  while (__any_sync(mask, miss)) {
+    unsigned long long w0[N], w1[N];
 #pragma unroll
-    for (int t = 0; t < kProbe; ++t) {
-      if (t < m) {
-        c[t] = __ldg(A.col + g + t);
-        if (jv::mbox_try(A.mbox, c[t], A.epoch, v[t])) ready |= 1u << t;
+    for (int t = 0; t < N; ++t)
+      if (miss & (1u << t))
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(w0[t]), "=l"(w1[t]) : "l"(A.mbox + 2 * (long long)c[t]));
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+      if ((miss & (1u << t)) && (uint32_t)(w0[t] >> 32) == A.epoch &&
+          (uint32_t)(w1[t] >> 32) == A.epoch) {
+        v[t] = __longlong_as_double((long long)((w0[t] & 0xffffffffull) | (w1[t] << 32)));
+        miss &= ~(1u << t);
       }
     }
-#pragma unroll
-    for (int t = 0; t < kProbe; ++t) {
-      if (t < m) {
-        if (!(ready & (1u << t))) v[t] = jv::mbox_wait(A.mbox, c[t], A.epoch);
-        s = jv::dsub(s, jv::dmul(__ldg(A.val + g + t), v[t]));
+    if (__any_sync(mask, miss)) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(2 * ns, 128u) : 16u;
+      if (++spins == jv::g_spin_limit) {
+        atomicExch(&jv::g_hang, 1);
+        break;
       }
+    }
+  }
+}
+
+// thread path: s -= val[p] * v[col[p]] over p in [p0, p1), ascending, kProbe
+// dependencies per round; `mask` = the lanes taking this path
+JV_INLINE double fold_deps(const SolveArgs& A, int p0, int p1, double s, unsigned mask) {
+  const int nch = (p1 - p0 + kProbe - 1) / kProbe;
+  const int maxch = __reduce_max_sync(mask, (unsigned)nch);
+  for (int ch = 0; ch < maxch; ++ch) {
+    const int g = p0 + ch * kProbe;
+    const int m = max(0, min(kProbe, p1 - g));
+    int c[kProbe];
+    double v[kProbe];
+#pragma unroll
+    for (int t = 0; t < kProbe; ++t) c[t] = (t < m) ? __ldg(A.col + g + t) : 0;
+    gather_conv<kProbe>(A, c, v, m ? (1u << m) - 1 : 0u, mask);
+#pragma unroll
+    for (int t = 0; t < kProbe; ++t)
+      if (t < m) s = jv::dsub(s, jv::dmul(__ldg(A.val + g + t), v[t]));
+  }
+  return s;
+}
+
+// warp path: same chain, 32 dependencies per round (lane t gathers one,
+// products formed in parallel, one lane keeps the subtraction order)
+JV_INLINE double fold_deps_warp(const SolveArgs& A, int p0, int p1, double s, int lane) {
+  const unsigned full = 0xffffffffu;
+  for (int g = p0; g < p1; g += 32) {
+    const int p = g + lane;
+    int c[1] = {p < p1 ? __ldg(A.col + p) : 0};
+    double v[1] = {0.0};
+    gather_conv<1>(A, c, v, p < p1 ? 1u : 0u, full);
+    const double prod = p < p1 ? jv::dmul(__ldg(A.val + p), v[0]) : 0.0;
+    const int m = min(32, p1 - g);
+    for (int t = 0; t < m; ++t) {
+      const double pt = __shfl_sync(full, prod, t);
+      s = jv::dsub(s, pt);
     }
   }
   return s;
 }
 
-__global__ void __launch_bounds__(256) solve_forward_kernel(SolveArgs A) {
+template <bool kBackward>
+__global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
+  const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int W = (gridDim.x * blockDim.x) >> 5;
-  for (int b = gw; b < A.nbatch; b += W) {
+  for (;;) {
+    const int b = jv::ticket_next(A.ticket, lane);
+    if (b >= A.nbatch) break;
     const int lo = A.batch_ptr[b], hi = A.batch_ptr[b + 1];
-    if (lo + lane >= hi) continue;
-    const int r = A.order[lo + lane];
-    const int rs = __ldg(A.row_start + r);
-    // strictly-lower part = columns < r; diag_pos marks its end
-    const int pe = __ldg(A.diag + r);
-    double s = A.in[r];
-    s = fold_deps(A, rs, pe, s);
-    A.out[r] = s;
-    jv::mbox_put(A.mbox, r, s, A.epoch);
+    const bool active = lo + lane < hi;
+    const int r = active ? A.order[lo + lane] : 0;
+    // dependency range: forward [rs, diag), backward (diag, re)
+    int p0 = 0, p1 = 0, dp = 0;
+    if (active) {
+      dp = __ldg(A.diag + r);
+      if (kBackward) { p0 = dp + 1; p1 = __ldg(A.row_start + r + 1); }
+      else { p0 = __ldg(A.row_start + r); p1 = dp; }
+    }
+    // gate: the newest dependency of the batch (forward: the largest column;
+    // backward: the smallest column > r)
+    int g;
+    if (kBackward) {
+      g = (active && p1 > p0) ? __ldg(A.col + p0) : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g = min(g, __shfl_xor_sync(full, g, o));
+      if (lane == 0 && g != 0x7fffffff) jv::mbox_gate(A.mbox, g, A.epoch);
+    } else {
+      g = (active && p1 > p0) ? __ldg(A.col + p1 - 1) : -1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g = max(g, __shfl_xor_sync(full, g, o));
+      if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, g, A.epoch);
+    }
+    __syncwarp();
+    const bool small = p1 - p0 <= kThreadDeps;
+    const unsigned smask = __ballot_sync(full, active && small);
+    if (active && small) {
+      double s = fold_deps(A, p0, p1, A.in[r], smask);
+      if (kBackward) s = jv::ddiv(s, __ldg(A.val + dp));
+      A.out[r] = s;
+      jv::mbox_put(A.mbox, r, s, A.epoch);
+    }
+    unsigned pend = __ballot_sync(full, active && !small);
+    while (pend) {
+      const int src = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const int rr = __shfl_sync(full, r, src);
+      const int q0 = __shfl_sync(full, p0, src), q1 = __shfl_sync(full, p1, src);
+      double s = fold_deps_warp(A, q0, q1, A.in[rr], lane);
+      if (lane == 0) {
+        if (kBackward) s = jv::ddiv(s, __ldg(A.val + __ldg(A.diag + rr)));
+        A.out[rr] = s;
+        jv::mbox_put(A.mbox, rr, s, A.epoch);
+      }
+      __syncwarp();
+    }
   }
-}
-
-__global__ void __launch_bounds__(256) solve_backward_kernel(SolveArgs A) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  for (int b = gw; b < A.nbatch; b += W) {
-    const int lo = A.batch_ptr[b], hi = A.batch_ptr[b + 1];
-    if (lo + lane >= hi) continue;
-    const int r = A.order[lo + lane];
-    const int dp = __ldg(A.diag + r);
-    const int re = __ldg(A.row_start + r + 1);
-    double s = A.in[r];
-    s = fold_deps(A, dp + 1, re, s);
-    const double x = jv::ddiv(s, __ldg(A.val + dp));
-    A.out[r] = x;
-    jv::mbox_put(A.mbox, r, x, A.epoch);
-  }
+  jv::ticket_exit(A.ticket, lane, W);
 }
 
 __global__ void check_zero_diag_kernel(int n, const double* val, const int32_t* diag, int32_t* row) {
@@ -102,23 +176,31 @@ __global__ void check_zero_diag_kernel(int n, const double* val, const int32_t* 
     if (val[diag[r]] == 0.0) atomicMin(row, r);
 }
 
+__global__ void classify_solve_kernel(int n, const int32_t* rs, const int32_t* diag, int backward,
+                                      int32_t* cls) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int deps = backward ? rs[r + 1] - diag[r] - 1 : diag[r] - rs[r];
+    cls[r] = deps > kThreadDeps ? 1 : 0;
+  }
+}
+
 }  // namespace
 
 extern "C" int jv_solve(int which, int32_t n, const int32_t* row_start, const int32_t* col,
                         const double* val, const int32_t* diag_pos, const int32_t* order,
                         const int32_t* batch_ptr, int32_t nbatch, const double* in, double* out,
-                        uint64_t* mbox, uint32_t epoch, void* stream) {
+                        uint64_t* mbox, uint32_t epoch, int32_t* ticket, void* stream) {
   if (n < 0 || nbatch < 0 || epoch == 0 || (which != 0 && which != 1)) {
     jvh::set_error("jv_solve: bad argument (which=%d n=%d nbatch=%d epoch=%u)", which, n,
                    nbatch, epoch);
     return JV_EINVAL;
   }
   if (n == 0 || nbatch == 0) return JV_OK;
-  SolveArgs A{row_start, col, val, diag_pos, order, batch_ptr, nbatch, in, out, mbox, epoch};
+  SolveArgs A{row_start, col, val, diag_pos, order, batch_ptr, nbatch, in, out, mbox, epoch, ticket};
   void* args[] = {&A};
   if (which == 0)
-    return jvh::coop_launch(solve_forward_kernel, 256, args, (cudaStream_t)stream, "jv_solve fwd");
-  return jvh::coop_launch(solve_backward_kernel, 256, args, (cudaStream_t)stream, "jv_solve bwd");
+    return jvh::persistent_launch(solve_kernel<false>, 256, args, (cudaStream_t)stream, "jv_solve fwd");
+  return jvh::persistent_launch(solve_kernel<true>, 256, args, (cudaStream_t)stream, "jv_solve bwd");
 }
 
 extern "C" int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,
@@ -128,5 +210,14 @@ extern "C" int jv_check_zero_diag(int32_t n, const double* val, const int32_t* d
   if (grid > 4 * jvh::sm_count()) grid = 4 * jvh::sm_count();
   check_zero_diag_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, val, diag_pos, row);
   JV_CHECK_LAUNCH("jv_check_zero_diag");
+  return JV_OK;
+}
+
+extern "C" int jv_classify_solve(int which, int32_t n, const int32_t* row_start,
+                                 const int32_t* diag_pos, int32_t* cls, void* stream) {
+  if (n <= 0) return JV_OK;
+  classify_solve_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, row_start, diag_pos,
+                                                                         which, cls);
+  JV_CHECK_LAUNCH("jv_classify_solve");
   return JV_OK;
 }

@@ -198,33 +198,45 @@ def batches_dev(nlev, level_ptr, n):
 
 @dataclass
 class Schedule:
-    """Level-batched row order for a sync-free sweep."""
+    """Level-batched row order for a sync-free sweep (jv_build_schedule):
+    keys = 2*level + class; class 0 rows 32 per batch, class 1 one each."""
 
     order: object
     batch_ptr: object
     nbatch: int
-    nlev: int
+    nkeys: int
+    keys: object = None      # per-row key (indexed by row id)
 
-    def restrict(self, lo, hi, level_of):
-        """Rows with lo <= index < hi, keeping the level batching."""
+    def restrict(self, lo, hi):
+        """Rows with lo <= index < hi, keeping level order and classes."""
         t = torch()
-        sel = self.order[(self.order >= lo) & (self.order < hi)].contiguous()
-        if sel.numel() == 0:
-            return Schedule(sel, empty_i32(1), 0, 0)
-        lev = level_of[sel.long()].long()
-        counts = t.bincount(lev, minlength=self.nlev)
-        level_ptr = t.zeros(self.nlev + 1, dtype=t.int64, device="cuda")
-        level_ptr[1:] = t.cumsum(counts, 0)
-        level_ptr = level_ptr.to(t.int32)
-        bp, nb = batches_dev(self.nlev, level_ptr, sel.numel())
-        return Schedule(sel, bp, nb, self.nlev)
+        rows = t.arange(lo, hi, dtype=t.int32, device="cuda")
+        keys = self.keys[lo:hi].contiguous()
+        return build_schedule(rows, keys, self.nkeys)
 
 
-def schedule_dev(a: DevCsr, backward: bool):
+def build_schedule(rows, keys, nkeys):
+    m = int(keys.numel())
+    order = empty_i32(m)
+    batch_ptr = empty_i32(m + nkeys + 2)
+    nb = ctypes.c_int32(0)
+    _lib.call("jv_build_schedule", m, ptr(rows), ptr(keys), int(nkeys), ptr(order),
+              ptr(batch_ptr), ctypes.byref(nb), stream())
+    return Schedule(order, batch_ptr, int(nb.value), nkeys)
+
+
+def schedule_dev(a: DevCsr, backward: bool, cls=None):
+    """Schedule of a sweep over pattern `a`: its levels (forward: columns <
+    r, backward: columns > r) plus per-row classes (None = all thread path)."""
+    t = torch()
     level_of, nlev = levels_dev(a, backward)
-    order, level_ptr = level_sort_dev(a.n, nlev, level_of)
-    bp, nb = batches_dev(nlev, level_ptr, a.n)
-    return Schedule(order, bp, nb, nlev), level_of
+    keys = level_of.to(t.int32) * 2
+    if cls is not None:
+        keys = keys + cls
+    keys = keys.contiguous()
+    sched = build_schedule(None, keys, 2 * max(nlev, 1))
+    sched.keys = keys
+    return sched, level_of
 
 
 # --------------------------------------------------------- ILU factors
@@ -249,11 +261,15 @@ class DevIlu:
         self.pattern = DevCsr(self.n, self.nnz, row_start, col)
         self._fwd = None
         self._bwd = None
+        self._fsched = None
+        self._fsched_milu = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
         self.fbox = Mailbox(self.nnz, 2)
         self.sbox = Mailbox(self.n, 2)
         self.err = reset_row_slot()
+        # batch tickets of the factor and solve kernels (kernels leave them 0)
+        self.ticket = torch().zeros(4, dtype=torch().int32, device="cuda")
 
     @staticmethod
     def from_host(n, row_start, col, diag_pos, val, tau=0.0, milu=False):
@@ -262,14 +278,31 @@ class DevIlu:
                       tau, milu)
 
     # schedules --------------------------------------------------------
+    def _classes(self, kind):
+        cls = empty_i32(self.n)
+        if kind == "factor":
+            _lib.call("jv_classify_factor", self.n, ptr(self.row_start), ptr(self.col),
+                      ptr(self.diag_pos), int(self.milu), ptr(cls), stream())
+        else:
+            _lib.call("jv_classify_solve", 0 if kind == "fwd" else 1, self.n,
+                      ptr(self.row_start), ptr(self.diag_pos), ptr(cls), stream())
+        return cls
+
+    def factor_schedule(self):
+        if self._fsched is None or self._fsched_milu != self.milu:
+            self._fsched, self._fwd_levels = schedule_dev(self.pattern, False,
+                                                          self._classes("factor"))
+            self._fsched_milu = self.milu
+        return self._fsched
+
     def fwd_schedule(self):
         if self._fwd is None:
-            self._fwd, self._fwd_levels = schedule_dev(self.pattern, False)
+            self._fwd, _ = schedule_dev(self.pattern, False, self._classes("fwd"))
         return self._fwd
 
     def bwd_schedule(self):
         if self._bwd is None:
-            self._bwd, _ = schedule_dev(self.pattern, True)
+            self._bwd, _ = schedule_dev(self.pattern, True, self._classes("bwd"))
         return self._bwd
 
     # numerics ---------------------------------------------------------
@@ -280,16 +313,16 @@ class DevIlu:
     def factor_async(self, lo=0, hi=None, ready_below=0, norms=True):
         """Launch the factorization of rows [lo, hi) (all by default)."""
         hi = self.n if hi is None else hi
-        sched = self.fwd_schedule()
+        sched = self.factor_schedule()
         if lo > 0 or hi < self.n:
-            sched = sched.restrict(lo, hi, self._fwd_levels)
+            sched = sched.restrict(lo, hi)
         if norms:
             self.compute_norms()
         _lib.call("jv_reset_row", ptr(self.err), stream())
         _lib.call("jv_factor", self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
                   ptr(self.diag_pos), ptr(self.norms), self.tau, int(self.milu), ptr(sched.order),
                   ptr(sched.batch_ptr), sched.nbatch, int(ready_below), ptr(self.fbox.buf),
-                  self.fbox.next_epoch(), ptr(self.err), stream())
+                  self.fbox.next_epoch(), ptr(self.err), ptr(self.ticket), stream())
 
     def factor(self, lo=0, hi=None, ready_below=0):
         """Factor and return the smallest zero-pivot row (or -1)."""
@@ -308,7 +341,8 @@ class DevIlu:
         sched = self.fwd_schedule() if which == 0 else self.bwd_schedule()
         _lib.call("jv_solve", which, self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
                   ptr(self.diag_pos), ptr(sched.order), ptr(sched.batch_ptr), sched.nbatch,
-                  ptr(b), ptr(out), ptr(self.sbox.buf), self.sbox.next_epoch(), stream())
+                  ptr(b), ptr(out), ptr(self.sbox.buf), self.sbox.next_epoch(),
+                  ctypes.c_void_p(self.ticket.data_ptr() + 8), stream())
         return out
 
     def host_val(self):

@@ -124,7 +124,7 @@ __global__ void gridbar(int K, unsigned int* bar) {
   }
 }
 
-int main() {
+int main1() {
   int dev = 0; cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, dev));
   printf("device %s SMs %d clock %d kHz\n", prop.name, prop.multiProcessorCount, prop.clockRate);
   const int K = 20000;
@@ -174,4 +174,36 @@ int main() {
   }
   CK(cudaGetLastError());
   return 0;
+}
+
+// ---- appended: __nanosleep granularity and a probe round trip
+__global__ void sleep_probe(unsigned ns, int reps, long long* out) {
+  long long t0 = clock64();
+  for (int i = 0; i < reps; ++i) __nanosleep(ns);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / reps;
+}
+__global__ void ldrelaxed_latency(const unsigned long long* p, int reps, long long* out) {
+  unsigned long long a = 0, b = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < reps; ++i) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p + ((a & 1) << 4)) : "memory");
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / reps + (long long)(a & 0);
+}
+int main2() {
+  long long* out; cudaMalloc(&out, 8); long long h;
+  unsigned long long* buf; cudaMalloc(&buf, 4096); cudaMemset(buf, 0, 4096);
+  for (unsigned ns : {0u, 16u, 64u, 256u, 1024u}) {
+    sleep_probe<<<1, 32>>>(ns, 1000, out); cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
+    printf("__nanosleep(%u): %lld cycles per call\n", ns, h);
+  }
+  ldrelaxed_latency<<<1, 32>>>(buf, 1000, out); cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
+  printf("ld.relaxed.gpu.v2 dependent latency: %lld cycles\n", h);
+  return 0;
+}
+int main(int argc, char** argv) {
+  if (argc > 1) return main2();
+  return main1();
 }
