@@ -71,6 +71,7 @@ struct WarpArena {
   int opw[kWarpOps];
   double opv[kWarpOps];
   int opend[32];
+  int pivc[32];
 };
 
 // lower_bound of key in arr[lo, hi)
@@ -253,7 +254,7 @@ JV_INLINE bool short_structure(const FactorArgs& A, int r, ShortRow& R, Slice S)
 // lane re-probes only its still-missing packets, then the warp votes; lanes
 // never spin on their own (divergent per-lane spin loops inside one warp
 // were measured to stretch a hop to ~20 us on config 2).
-JV_INLINE void short_gather(const FactorArgs& A, const ShortRow& R, Slice S, unsigned mask) {
+JV_INLINE unsigned short_gather(const FactorArgs& A, const ShortRow& R, Slice S, unsigned mask) {
   constexpr int kSlots = kP * (kU + 1);
   // slot (k, u): u = 0 the pivot's diagonal, u > 0 its u-th upper entry;
   // R.miss was prepared before the gate (pivots factored by an earlier call
@@ -262,8 +263,9 @@ JV_INLINE void short_gather(const FactorArgs& A, const ShortRow& R, Slice S, uns
   int dq[kP];
 #pragma unroll
   for (int k = 0; k < kP; ++k) dq[k] = S.dq(k);
-  unsigned ns = 0, spins = 0;
+  unsigned ns = 0, spins = 0, rounds = 0;
   while (__any_sync(mask, miss)) {
+    ++rounds;
     Probe p[kSlots];
 #pragma unroll
     for (int sl = 0; sl < kSlots; ++sl)
@@ -285,12 +287,16 @@ JV_INLINE void short_gather(const FactorArgs& A, const ShortRow& R, Slice S, uns
       }
     }
   }
+  return rounds;
 }
 
 JV_INLINE void short_finish(const FactorArgs& A, int r, const ShortRow& R, Slice S,
-                            unsigned mask, int cur_batch) {
-  short_gather(A, R, S, mask);
-  if ((threadIdx.x & 31) == __ffs(mask) - 1) jv::trace_mark(cur_batch, 7);
+                            unsigned mask, int cur_batch, const jv::Trace& T) {
+  const unsigned rounds = short_gather(A, R, S, mask);
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) {
+    jv::trace_mark(T, cur_batch, 7);
+    jv::trace_word(T, cur_batch, 8, rounds);
+  }
   // divisions of untouched pivots: independent, issued together
   double ls[kP];
 #pragma unroll
@@ -314,7 +320,7 @@ JV_INLINE void short_finish(const FactorArgs& A, int r, const ShortRow& R, Slice
       o = oe;
     }
   }
-  if ((threadIdx.x & 31) == __ffs(mask) - 1) jv::trace_mark2(cur_batch);
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) jv::trace_mark2(T, cur_batch);
   for (int i = 0; i < R.len; ++i) {
     const double v = S.a(i);
     __stcg(A.val + R.rs + i, v);
@@ -323,7 +329,198 @@ JV_INLINE void short_finish(const FactorArgs& A, int r, const ShortRow& R, Slice
   if (S.a(R.nL) == 0.0) atomicMin(A.err, r);
 }
 
+// ------------------------------------------------------ stencil fast path
+//
+// A short row whose pivots' U rows meet the row ONLY at its diagonal (every
+// 5/7-point stencil row under ILU(0): the grid graph has no triangles) has
+// independent pivots and a single update target.  Its strictly-upper
+// entries are final from the start, so they are published before the gate;
+// after the gate the row needs 2 packets per pivot, one division per pivot
+// (all independent) and the diagonal's subtraction chain — everything in
+// registers.
+
+struct SfpRow {
+  int rs, nL, dp;
+  double aL[kP];      // strict-lower values
+  double adiag;
+  int dq[kP];         // pivot diagonal positions
+  int us[kP];         // position of u(c_k, r) (-1: none)
+  double dv[kP], uv[kP];   // values of pivots factored by an earlier call
+  unsigned old;       // bit k: pivot k read from val[] (ready_below)
+  double thresh;
+  int gate, gate_q;
+};
+
+JV_INLINE bool sfp_structure(const FactorArgs& A, int r, SfpRow& F) {
+  F.rs = __ldg(A.row_start + r);
+  const int len = __ldg(A.row_start + r + 1) - F.rs;
+  F.dp = __ldg(A.diag + r);
+  F.nL = F.dp - F.rs;
+  F.gate = -1;
+  F.gate_q = 0;
+  F.old = 0;
+  if (len > kR || F.nL > kP || A.milu) return false;
+  int cj[kR];
+  double a[kR];
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    cj[i] = (i < len) ? __ldg(A.col + F.rs + i) : -1;
+    a[i] = (i < len) ? __ldcs(A.val + F.rs + i) : 0.0;
+  }
+  int ce[kP];
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    F.dq[k] = (k < F.nL) ? __ldg(A.diag + cj[k]) : 0;
+    ce[k] = (k < F.nL) ? __ldg(A.row_start + cj[k] + 1) : 1;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) ok &= ce[k] - F.dq[k] - 1 <= kU;
+  if (!ok) return false;
+  int uc[kP][kU];
+#pragma unroll
+  for (int k = 0; k < kP; ++k)
+#pragma unroll
+    for (int t = 0; t < kU; ++t)
+      uc[k][t] = (k < F.nL && t < ce[k] - F.dq[k] - 1) ? __ldg(A.col + F.dq[k] + 1 + t) : -2;
+  // every U entry of every pivot must miss the row, except at column r
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    F.us[k] = -1;
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      const int j = uc[k][t];
+      if (j == r) F.us[k] = F.dq[k] + 1 + t;
+#pragma unroll
+      for (int i = 0; i < kR; ++i) ok &= !(j >= 0 && j != r && cj[i] == j);
+    }
+  }
+  if (!ok) return false;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) F.aL[k] = a[k];
+  F.adiag = 0.0;
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    if (i == F.nL) F.adiag = a[i];
+    // strictly-upper entries are final: publish them now
+    if (i > F.nL && i < len) jv::mbox_put(A.mbox, F.rs + i, a[i], A.epoch);
+  }
+  F.thresh = (A.tau > 0.0) ? jv::dmul(A.tau, __ldg(A.norms + r)) : 0.0;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    if (k < F.nL && cj[k] < A.ready_below) {
+      F.old |= 1u << k;
+      F.dv[k] = __ldcg(A.val + F.dq[k]);
+      F.uv[k] = F.us[k] >= 0 ? __ldcg(A.val + F.us[k]) : 0.0;
+    }
+  }
+  if (F.nL > 0) {
+    int c = -1, q = 0;
+#pragma unroll
+    for (int k = 0; k < kP; ++k)
+      if (k < F.nL) { c = cj[k]; q = F.dq[k]; }
+    if (c >= A.ready_below) { F.gate = c; F.gate_q = q; }
+  }
+  return true;
+}
+
+// finishing a row once all its inputs are in: parallel divisions, the
+// diagonal chain, stores and the diagonal's packet
+JV_INLINE void sfp_compute(const FactorArgs& A, int r, SfpRow& F) {
+  double l[kP];
+#pragma unroll
+  for (int k = 0; k < kP; ++k) l[k] = (k < F.nL) ? jv::ddiv(F.aL[k], F.dv[k]) : 0.0;
+  double d = F.adiag;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    if (k < F.nL) {
+      const bool drop = A.tau > 0.0 && fabs(l[k]) < F.thresh;
+      if (drop) l[k] = 0.0;
+      else if (F.us[k] >= 0) d = jv::dsub(d, jv::dmul(l[k], F.uv[k]));
+    }
+  }
+  jv::mbox_put(A.mbox, F.dp, d, A.epoch);
+#pragma unroll
+  for (int k = 0; k < kP; ++k)
+    if (k < F.nL) __stcg(A.val + F.rs + k, l[k]);
+  __stcg(A.val + F.dp, d);
+  if (d == 0.0) atomicMin(A.err, r);
+}
+
+// Gather of the pivots' diagonals and u(c_k, r), warp-converged (no lane
+// spins alone), then the row is finished.  (Finishing each lane inside the
+// loop as soon as its own inputs arrive was measured slower on config 2:
+// the divergent compute inside the polling loop costs more than the
+// coupling it removes.)
+JV_INLINE void sfp_finish(const FactorArgs& A, int r, SfpRow& F, unsigned mask, int cur_batch,
+                          const jv::Trace& T) {
+  unsigned miss = 0;
+#pragma unroll
+  for (int k = 0; k < kP; ++k)
+    if (k < F.nL && !(F.old & (1u << k))) miss |= (F.us[k] >= 0 ? 3u : 1u) << (2 * k);
+  unsigned ns = 0, spins = 0;
+  while (__any_sync(mask, miss)) {
+    Probe p[2 * kP];
+#pragma unroll
+    for (int k = 0; k < kP; ++k) {
+      if (miss & (1u << (2 * k))) p[2 * k] = probe_issue(A.mbox, F.dq[k]);
+      if (miss & (2u << (2 * k))) p[2 * k + 1] = probe_issue(A.mbox, F.us[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k) {
+      if ((miss & (1u << (2 * k))) && probe_ok(p[2 * k], A.epoch)) {
+        F.dv[k] = probe_val(p[2 * k]);
+        miss &= ~(1u << (2 * k));
+      }
+      if ((miss & (2u << (2 * k))) && probe_ok(p[2 * k + 1], A.epoch)) {
+        F.uv[k] = probe_val(p[2 * k + 1]);
+        miss &= ~(2u << (2 * k));
+      }
+    }
+    if (__any_sync(mask, miss)) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(2 * ns, 128u) : 16u;
+      if (++spins == jv::g_spin_limit) {
+        atomicExch(&jv::g_hang, 1);
+        break;
+      }
+    }
+  }
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) jv::trace_mark(T, cur_batch, 7);
+  sfp_compute(A, r, F);
+}
+
 // ------------------------------------------------------------------ warp path
+
+// Warp-converged wait for one packet per lane (lanes with need == false
+// just vote): no lane ever spins alone.
+JV_INLINE double warp_value(const FactorArgs& A, bool need, int c, int q) {
+  double v = 0.0;
+  bool miss = need;
+  if (need && c < A.ready_below) {
+    v = __ldcg(A.val + q);
+    miss = false;
+  }
+  unsigned ns = 0, spins = 0;
+  while (__any_sync(0xffffffffu, miss)) {
+    if (miss) {
+      const Probe p = probe_issue(A.mbox, q);
+      if (probe_ok(p, A.epoch)) {
+        v = probe_val(p);
+        miss = false;
+      }
+    }
+    if (__any_sync(0xffffffffu, miss)) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(2 * ns, 128u) : 16u;
+      if (++spins == jv::g_spin_limit) {
+        atomicExch(&jv::g_hang, 1);
+        break;
+      }
+    }
+  }
+  return v;
+}
 
 // Apply all pivots of row r with the whole warp.
 JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
@@ -342,7 +539,7 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
     }
     __syncwarp();
   }
-  const double thresh = jv::dmul(A.tau, A.norms[r]);
+  const double thresh = A.tau > 0.0 ? jv::dmul(A.tau, A.norms[r]) : 0.0;
 
   for (int k0 = 0; k0 < nL;) {
     const int kc = min(32, nL - k0);
@@ -351,6 +548,7 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
       c = ac[k0 + lane];
       d = A.diag[c];
       ce = A.row_start[c + 1];
+      W.pivc[lane] = c;
     }
     // ---- structure of the chunk: op list (q, target) per pivot
     int nops = 0, kdone = 0;
@@ -364,14 +562,16 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
         if (kk == 0) direct = true;   // a single pivot larger than the list
         break;
       }
-      if (A.milu) {
+      if (A.milu || ulen <= rem) {
+        // lanes over U(c), each searched in the rest of this row
         for (int base = dk + 1; base < cek; base += 32) {
           const int q = base + lane;
           int w = -1;
           if (q < cek) {
             const int j = A.col[q];
             const int p = lower_bound(ac, k + 1, len, j);
-            w = (p < len && ac[p] == j) ? p : (dloc | kOut);
+            if (p < len && ac[p] == j) w = p;
+            else if (A.milu) w = dloc | kOut;
           }
           const unsigned m = __ballot_sync(full, w >= 0);
           if (w >= 0) {
@@ -381,7 +581,8 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
           }
           nops += __popc(m);
         }
-      } else if (ulen > rem) {
+      } else {
+        // long pivot row: lanes over this row's rest, each searched in U(c)
         for (int base = k + 1; base < len; base += 32) {
           const int w = base + lane;
           int q = -1;
@@ -397,23 +598,6 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
           }
           nops += __popc(m);
         }
-      } else {
-        for (int base = dk + 1; base < cek; base += 32) {
-          const int q = base + lane;
-          int w = -1;
-          if (q < cek) {
-            const int j = A.col[q];
-            const int p = lower_bound(ac, k + 1, len, j);
-            if (p < len && ac[p] == j) w = p;
-          }
-          const unsigned m = __ballot_sync(full, w >= 0);
-          if (w >= 0) {
-            const int pos = nops + __popc(m & ((1u << lane) - 1));
-            W.opq[pos] = q;
-            W.opw[pos] = w;
-          }
-          nops += __popc(m);
-        }
       }
       if (lane == 0) W.opend[kk] = nops;
       kdone = kk + 1;
@@ -421,14 +605,15 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
     __syncwarp();
 
     if (direct) {
-      // one pivot whose updates exceed the op list: wait and apply in place
+      // one pivot whose updates exceed the op list: stream it in blocks of 32
       const int k = k0;
       const int dk = __shfl_sync(full, d, 0), cek = __shfl_sync(full, ce, 0);
       const int ck = __shfl_sync(full, c, 0);
+      const double piv = warp_value(A, lane == 0, ck, dk);
       double l = 0.0;
       int drop = 0;
       if (lane == 0) {
-        l = jv::ddiv(av[k], pivot_value(A, ck, dk));
+        l = jv::ddiv(av[k], piv);
         drop = A.tau > 0.0 && fabs(l) < thresh;
         av[k] = drop ? 0.0 : l;
       }
@@ -437,29 +622,47 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
       __syncwarp();
       const int ulen = cek - dk - 1, rem = len - k - 1;
       if (A.milu) {
-        if (lane == 0) {
-          int w = k + 1;
-          for (int q = dk + 1; q < cek; ++q) {
-            const double u = pivot_value(A, ck, q);
-            if (drop) { av[dloc] = jv::dsub(av[dloc], jv::dmul(l, u)); continue; }
+        // diagonal contributions in q order: lane 0 folds each block in order
+        for (int base = dk + 1; base < cek; base += 32) {
+          const int q = base + lane;
+          int w = dloc;
+          if (q < cek && !drop) {
             const int j = A.col[q];
-            while (w < len && ac[w] < j) ++w;
-            const int t = (w < len && ac[w] == j) ? w : dloc;
-            av[t] = jv::dsub(av[t], jv::dmul(l, u));
+            const int p = lower_bound(ac, k + 1, len, j);
+            if (p < len && ac[p] == j) w = p;
           }
+          const double u = warp_value(A, q < cek, ck, q);
+          const double prod = jv::dmul(l, u);
+          for (int t = 0; t < 32 && base + t < cek; ++t) {
+            const double pt = __shfl_sync(full, prod, t);
+            const int wt = __shfl_sync(full, w, t);
+            if (lane == 0) av[wt] = jv::dsub(av[wt], pt);
+          }
+          __syncwarp();
         }
       } else if (!drop) {
         if (ulen > rem) {
-          for (int w = k + 1 + lane; w < len; w += 32) {
-            const int p = lower_bound(A.col, dk + 1, cek, ac[w]);
-            if (p < cek && A.col[p] == ac[w])
-              av[w] = jv::dsub(av[w], jv::dmul(l, pivot_value(A, ck, p)));
+          for (int base = k + 1; base < len; base += 32) {
+            const int w = base + lane;
+            int p = -1;
+            if (w < len) {
+              const int pp = lower_bound(A.col, dk + 1, cek, ac[w]);
+              if (pp < cek && A.col[pp] == ac[w]) p = pp;
+            }
+            const double u = warp_value(A, p >= 0, ck, p);
+            if (p >= 0) av[w] = jv::dsub(av[w], jv::dmul(l, u));
           }
         } else {
-          for (int q = dk + 1 + lane; q < cek; q += 32) {
-            const int j = A.col[q];
-            const int p = lower_bound(ac, k + 1, len, j);
-            if (p < len && ac[p] == j) av[p] = jv::dsub(av[p], jv::dmul(l, pivot_value(A, ck, q)));
+          for (int base = dk + 1; base < cek; base += 32) {
+            const int q = base + lane;
+            int p = -1;
+            if (q < cek) {
+              const int j = A.col[q];
+              const int pp = lower_bound(ac, k + 1, len, j);
+              if (pp < len && ac[pp] == j) p = pp;
+            }
+            const double u = warp_value(A, p >= 0, ck, q);
+            if (p >= 0) av[p] = jv::dsub(av[p], jv::dmul(l, u));
           }
         }
       }
@@ -468,7 +671,7 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
       continue;
     }
 
-    // ---- gate on the newest pivot of the chunk, then gather
+    // ---- gate on the newest pivot of the chunk, then one converged gather
     int g = (lane < kdone && c >= A.ready_below) ? c : -1, gq = d;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -477,13 +680,22 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
     }
     if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, gq, A.epoch);
     __syncwarp();
-    double dv = 1.0;
-    if (lane < kdone) dv = pivot_value(A, c, d);
-    for (int kk = 0, o0 = 0; kk < kdone; ++kk) {
-      const int ck = __shfl_sync(full, c, kk);
-      const int o1 = W.opend[kk];
-      for (int o = o0 + lane; o < o1; o += 32) W.opv[o] = pivot_value(A, ck, W.opq[o]);
-      o0 = o1;
+    const double dv = warp_value(A, lane < kdone, c, d);
+    for (int base = 0; base < nops; base += 32) {
+      const int o = base + lane;
+      int ck = 0, q = 0;
+      if (o < nops) {
+        // pivot of op o: first kk with opend[kk] > o
+        int lo = 0, hi = kdone - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (W.opend[mid] > o) hi = mid; else lo = mid + 1;
+        }
+        ck = W.pivc[lo];
+        q = W.opq[o];
+      }
+      const double v = warp_value(A, o < nops, ck, q);
+      if (o < nops) W.opv[o] = v;
     }
     __syncwarp();
 
@@ -539,22 +751,28 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
   const int lane = threadIdx.x & 31;
   WarpArena& W = arena[threadIdx.x >> 5];
   const Slice S{(int)threadIdx.x};
+  const jv::Trace T = jv::trace_begin();
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (;;) {
-    const int b = jv::ticket_next(A.ticket, lane);
+    const int b = jv::ticket_next(A.ticket, lane, T);
     if (b >= A.nbatch) break;
     const int lo = A.batch_ptr[b], hi = A.batch_ptr[b + 1];
     const int idx = lo + lane;
     const bool active = idx < hi;
     const int r = active ? A.order[idx] : -1;
-    if (lane == 0) jv::trace_mark(b, 1);
+    if (lane == 0) jv::trace_mark(T, b, 1);
+    SfpRow F;
     ShortRow R;
-    bool fits = false;
-    if (active) fits = short_structure(A, r, R, S);
+    bool sfp = false, fits = false;
+    if (active) {
+      sfp = sfp_structure(A, r, F);
+      if (!sfp) fits = short_structure(A, r, R, S);
+    }
     __syncwarp();
-    if (lane == 0) jv::trace_mark(b, 2);
-    // warp gate on the newest pivot of the batch's short rows
-    int g = fits ? R.gate : -1, gq = fits ? R.gate_q : 0;
+    if (lane == 0) jv::trace_mark(T, b, 2);
+    // warp gate on the newest pivot of the batch's thread-path rows
+    int g = sfp ? F.gate : (fits ? R.gate : -1);
+    int gq = sfp ? F.gate_q : (fits ? R.gate_q : 0);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const int og = __shfl_xor_sync(full, g, o), oq = __shfl_xor_sync(full, gq, o);
@@ -562,17 +780,19 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
     }
     if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, gq, A.epoch);
     __syncwarp();
-    if (lane == 0) jv::trace_mark(b, 3);
+    if (lane == 0) jv::trace_mark(T, b, 3);
+    const unsigned smask = __ballot_sync(full, sfp);
+    if (sfp) sfp_finish(A, r, F, smask, b, T);
     const unsigned fmask = __ballot_sync(full, fits);
-    if (fits) short_finish(A, r, R, S, fmask, b);
-    unsigned pend = __ballot_sync(full, active && !fits);
+    if (fits) short_finish(A, r, R, S, fmask, b, T);
+    unsigned pend = __ballot_sync(full, active && !fits && !sfp);
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
       warp_row(A, __shfl_sync(full, r, src), lane, W);
     }
     __syncwarp();
-    if (lane == 0) jv::trace_mark(b, 4);
+    if (lane == 0) jv::trace_mark(T, b, 4);
   }
   jv::ticket_exit(A.ticket, lane, nw);
 }

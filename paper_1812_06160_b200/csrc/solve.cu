@@ -117,8 +117,9 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int W = (gridDim.x * blockDim.x) >> 5;
+  const jv::Trace T = jv::trace_begin();
   for (;;) {
-    const int b = jv::ticket_next(A.ticket, lane);
+    const int b = jv::ticket_next(A.ticket, lane, T);
     if (b >= A.nbatch) break;
     const int lo = A.batch_ptr[b], hi = A.batch_ptr[b + 1];
     const bool active = lo + lane < hi;
