@@ -64,6 +64,8 @@ int jv_set_backoff(unsigned cap_ns);
 /* diagnostics: record 4 globaltimer stamps per factor batch into buf
  * (device, 16*batches uint64; NULL disables) */
 int jv_set_trace(unsigned long long* buf, long long batches);
+/* test hook: out = a / b through the kernels' batched fast division */
+int jv_test_ddiv(int32_t n, const double* a, const double* b, double* out, void* stream);
 
 /* ---- spmv: y = A x ---------------------------------------------------
  * replaces _kernels.py:28-34 spmv_kernel (called by csr.py:251-260 spmv).
@@ -199,6 +201,30 @@ int jv_classify_factor(int32_t n, const int32_t* row_start, const int32_t* col,
                        const int32_t* diag_pos, int milu, int32_t* cls, void* stream);
 int jv_classify_solve(int which, int32_t n, const int32_t* row_start, const int32_t* diag_pos,
                       int32_t* cls, void* stream);
+
+/* ---- CTA-resident region factorization (stencil-class matrices) ------
+ * Setup (host C++): BFS-grown regions over the symmetrized pattern, rows
+ * ordered by level inside each region and cut into waves of
+ * jv_region_threads() rows (sign bit of wave_beg = level ends here);
+ * per-slot descriptors (returns the count of rows that are NOT
+ * stencil-class: the region kernel needs 0).  See csrc/region.cu. */
+int64_t jv_region_plan_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h,
+                            const int32_t* level_h, int32_t nreg, int32_t wave,
+                            int32_t* region_of_h, int32_t* slot_row_h, int32_t* slot_of_h,
+                            int32_t* reg_ptr_h, int32_t* wave_ptr_h, int32_t* wave_beg_h);
+int64_t jv_region_desc_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h,
+                            const int32_t* diag_h, const int32_t* region_of_h,
+                            const int32_t* slot_row_h, const int32_t* slot_of_h,
+                            const int32_t* reg_ptr_h, int32_t* info_h, int32_t* drs_h,
+                            int32_t* ref_h, int32_t* us_h);
+int jv_region_threads(void);
+/* replaces factor_serial_kernel (_kernels.py:197-204) for stencil-class
+ * matrices: one co-resident CTA per region, bitwise equal results */
+int jv_factor_regions(int32_t n, int32_t nreg, const int32_t* slot_row, const int32_t* info,
+                      const int32_t* drs, const int32_t* ref, const int32_t* us,
+                      const int32_t* reg_ptr, const int32_t* wave_ptr, const int32_t* wave_beg,
+                      int32_t max_region, double* val, const double* norms, double tau,
+                      uint64_t* mbox, uint32_t epoch, int32_t* err_row, void* stream);
 
 #ifdef __cplusplus
 }

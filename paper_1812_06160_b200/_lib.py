@@ -32,6 +32,7 @@ _SIGS = {
     "jv_set_spin_limit": [ctypes.c_uint],
     "jv_set_backoff": [ctypes.c_uint],
     "jv_set_trace": [_P, ctypes.c_longlong],
+    "jv_test_ddiv": [c_int32, _P, _P, _P, _P],
     "jv_spmv_tile": [],
     "jv_spmv_plan": [c_int32, c_int32, _P, _P, _P],
     "jv_spmv": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P],
@@ -56,11 +57,18 @@ _SIGS = {
     "jv_build_schedule": [c_int32, _P, _P, c_int32, _P, _P, _I32P, _P],
     "jv_classify_factor": [c_int32, _P, _P, _P, c_int, _P, _P],
     "jv_classify_solve": [c_int, c_int32, _P, _P, _P, _P],
+    "jv_region_plan_host": [c_int32, _P, _P, _P, c_int32, c_int32, _P, _P, _P, _P, _P, _P],
+    "jv_region_desc_host": [c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "jv_factor_regions": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, _P, _P,
+                          c_double, _P, c_uint32, _P, _P],
+    "jv_region_threads": [],
 }
 _RESTYPES = {
     "jv_last_error": ctypes.c_char_p,
     "jv_iluk_host": c_int64,
     "jv_free_host": None,
+    "jv_region_plan_host": c_int64,
+    "jv_region_desc_host": c_int64,
 }
 
 _lib = None

@@ -144,3 +144,23 @@ extern "C" int jv_status(int* hang_h) {
   if (hang_h) *hang_h = h;
   return JV_OK;
 }
+
+// Test hook: out[i] = ddiv_fast(a[i], b[i]) with the __ddiv_rn fallback, so
+// the parity tests can compare it with IEEE division bit for bit.
+namespace {
+__global__ void ddiv_test_kernel(int n, const double* a, const double* b, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    bool slow;
+    double q = jv::ddiv_fast(a[i], b[i], slow);
+    if (slow) q = __ddiv_rn(a[i], b[i]);
+    out[i] = q;
+  }
+}
+}  // namespace
+
+extern "C" int jv_test_ddiv(int32_t n, const double* a, const double* b, double* out, void* stream) {
+  if (n <= 0) return JV_OK;
+  ddiv_test_kernel<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256, 0, (cudaStream_t)stream>>>(n, a, b, out);
+  JV_CHECK_LAUNCH("jv_test_ddiv");
+  return JV_OK;
+}

@@ -428,8 +428,7 @@ JV_INLINE bool sfp_structure(const FactorArgs& A, int r, SfpRow& F) {
 // diagonal chain, stores and the diagonal's packet
 JV_INLINE void sfp_compute(const FactorArgs& A, int r, SfpRow& F) {
   double l[kP];
-#pragma unroll
-  for (int k = 0; k < kP; ++k) l[k] = (k < F.nL) ? jv::ddiv(F.aL[k], F.dv[k]) : 0.0;
+  jv::ddiv_batch<kP>(F.aL, F.dv, l, F.nL);
   double d = F.adiag;
 #pragma unroll
   for (int k = 0; k < kP; ++k) {

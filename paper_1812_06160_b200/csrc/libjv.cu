@@ -5,4 +5,5 @@
 #include "factor.cu"
 #include "solve.cu"
 #include "setup.cu"
+#include "region.cu"
 #include "host.cpp"

@@ -60,6 +60,72 @@ def f64(a):
     return t.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda")
 
 
+# ---- host <-> device transfers for the drop-in API ----------------------
+# numpy arrays are pageable; a pinned staging buffer lets the DMA run at full
+# link speed while torch's parallel host copy fills it chunk by chunk, so
+# the host copy of chunk i+1 overlaps the DMA of chunk i.
+
+_PIN = {}
+_CHUNK = 1 << 21   # doubles per chunk (16 MB)
+
+
+def _pinned(n):
+    """The staging buffer, once its previous DMA has drained."""
+    t = torch()
+    ev = _PIN.get("busy")
+    if ev is not None:
+        ev.synchronize()
+    buf = _PIN.get("f64")
+    if buf is None or buf.numel() < n:
+        buf = t.empty(max(n, 1), dtype=t.float64, pin_memory=True)
+        _PIN["f64"] = buf
+    return buf
+
+
+def _mark_busy():
+    ev = torch().cuda.Event()
+    ev.record()
+    _PIN["busy"] = ev
+
+
+def upload_f64(dst, src):
+    """dst (device tensor) <- src (host float64 numpy array)."""
+    t = torch()
+    src = np.ascontiguousarray(src, dtype=np.float64)
+    n = src.size
+    if n == 0:
+        return dst
+    pin = _pinned(n)
+    hsrc = t.from_numpy(src)
+    for a in range(0, n, _CHUNK):
+        b = min(n, a + _CHUNK)
+        pin[a:b].copy_(hsrc[a:b])
+        dst[a:b].copy_(pin[a:b], non_blocking=True)
+    _mark_busy()
+    return dst
+
+
+def download_f64(dst, src, n=None):
+    """dst (host float64 numpy array, written in place) <- src[:n] (device)."""
+    t = torch()
+    n = dst.size if n is None else n
+    if n == 0:
+        return dst
+    pin = _pinned(n)
+    hdst = t.from_numpy(dst)
+    events = []
+    for a in range(0, n, _CHUNK):
+        b = min(n, a + _CHUNK)
+        pin[a:b].copy_(src[a:b], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record()
+        events.append((a, b, ev))
+    for a, b, ev in events:
+        ev.synchronize()
+        hdst[a:b].copy_(pin[a:b])
+    return dst
+
+
 def empty_i32(n):
     return torch().empty(max(int(n), 1), dtype=torch().int32, device="cuda")
 
@@ -263,6 +329,7 @@ class DevIlu:
         self._bwd = None
         self._fsched = None
         self._fsched_milu = None
+        self._rplan = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
         self.fbox = Mailbox(self.nnz, 2)
@@ -310,9 +377,90 @@ class DevIlu:
         _lib.call("jv_row_norms", self.n, ptr(self.row_start), ptr(self.val), self.tau,
                   ptr(self.norms), stream())
 
+    # CTA-resident region plan (stencil-class matrices) --------------------
+    # Regions must be convex in the dependency order (grid-aligned boxes for
+    # a stencil): the caller supplies them as a row -> region map (a domain
+    # decomposition, in the factor's row numbering).  Without one, BFS-grown
+    # regions are tried only when use_regions is set: they follow the level
+    # sets and come out as slabs, which serialise (slower than tickets).
+    use_regions = False
+    region_hint = None
+
+    def set_regions(self, region_of):
+        """Region id per row (factor numbering), ids 0..R-1 with R <= #SMs."""
+        self.region_hint = np.ascontiguousarray(region_of, dtype=np.int32)
+        self._rplan = None
+
+    def region_plan(self):
+        """Host-built region plan (jv_region_plan_host / jv_region_desc_host)
+        uploaded once; None when some row is not stencil-class."""
+        if self._rplan is None:
+            self._rplan = self._build_region_plan() or False
+        return self._rplan or None
+
+    def _build_region_plan(self):
+        t = torch()
+        n = self.n
+        if n < 64:
+            return None
+        self.factor_schedule()
+        lib = _lib.load()
+        host = lambda x, m: np.ascontiguousarray(x[:m].cpu().numpy(), dtype=np.int32)
+        rs = host(self.row_start, n + 1)
+        col = host(self.col, self.nnz)
+        diag = host(self.diag_pos, n)
+        lev = host(self._fwd_levels, n)
+        sms = t.cuda.get_device_properties(t.cuda.current_device()).multi_processor_count
+        nreg = min(sms, max(1, n // 64))
+        if self.region_hint is not None:
+            nreg = int(self.region_hint.max()) + 1
+        wave = lib.jv_region_threads()
+        region_of = (self.region_hint.copy() if self.region_hint is not None
+                     else np.full(n, -1, np.int32))
+        slot_row = np.empty(n, np.int32)
+        slot_of = np.empty(n, np.int32)
+        reg_ptr = np.empty(nreg + 1, np.int32)
+        wave_ptr = np.empty(nreg + 1, np.int32)
+        nlev = int(lev.max()) + 1
+        wave_beg = np.empty(n + nlev * nreg + 1, np.int32)
+        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        nw = lib.jv_region_plan_host(n, P(rs), P(col), P(lev), nreg, wave, P(region_of),
+                                     P(slot_row), P(slot_of), P(reg_ptr), P(wave_ptr), P(wave_beg))
+        if nw < 0:
+            return None
+        info = np.empty(n, np.int32)
+        drs = np.empty(n, np.int32)
+        ref = np.empty(4 * n, np.int32)
+        us = np.empty(4 * n, np.int32)
+        bad = lib.jv_region_desc_host(n, P(rs), P(col), P(diag), P(region_of), P(slot_row),
+                                      P(slot_of), P(reg_ptr), P(info), P(drs), P(ref), P(us))
+        if bad != 0:
+            return None
+        max_region = int(np.diff(reg_ptr).max())
+        if max_region * 8 > 220 * 1024:
+            return None
+        up = lambda a: t.from_numpy(a).to("cuda")
+        return dict(nreg=nreg, max_region=max_region, slot_row=up(slot_row), info=up(info),
+                    drs=up(drs), ref=up(ref), us=up(us), reg_ptr=up(reg_ptr),
+                    wave_ptr=up(wave_ptr), wave_beg=up(wave_beg[:max(nw, 1)]),
+                    crossing=float(np.mean(ref[:n] < 0)))
+
     def factor_async(self, lo=0, hi=None, ready_below=0, norms=True):
         """Launch the factorization of rows [lo, hi) (all by default)."""
         hi = self.n if hi is None else hi
+        if (lo == 0 and hi == self.n and ready_below == 0 and not self.milu
+                and (self.use_regions or self.region_hint is not None)
+                and self.region_plan() is not None):
+            rp = self.region_plan()
+            if norms:
+                self.compute_norms()
+            _lib.call("jv_reset_row", ptr(self.err), stream())
+            _lib.call("jv_factor_regions", self.n, rp["nreg"], ptr(rp["slot_row"]),
+                      ptr(rp["info"]), ptr(rp["drs"]), ptr(rp["ref"]), ptr(rp["us"]),
+                      ptr(rp["reg_ptr"]), ptr(rp["wave_ptr"]), ptr(rp["wave_beg"]),
+                      rp["max_region"], ptr(self.val), ptr(self.norms), self.tau,
+                      ptr(self.fbox.buf), self.fbox.next_epoch(), ptr(self.err), stream())
+            return
         sched = self.factor_schedule()
         if lo > 0 or hi < self.n:
             sched = sched.restrict(lo, hi)

@@ -30,10 +30,16 @@ def row_inf_norms(factors: IluFactors) -> np.ndarray:
     return dv.host_f64(d.norms, factors.n)
 
 
-def _run(factors: IluFactors, lo=0, hi=None, ready_below=0) -> int:
+def _run(factors: IluFactors, lo=0, hi=None, ready_below=0, keep_after_bad=False) -> int:
     d = factors.upload_values()
     bad = d.factor(lo, hi, ready_below)
-    factors.val[:] = d.host_val()
+    n_out = factors.pattern.nnz
+    if bad >= 0 and keep_after_bad:
+        # the reference stops at the first zero pivot: rows after it keep
+        # their input values, which the host array still holds
+        n_out = int(factors.pattern.row_start[bad + 1])
+    factors.val = np.ascontiguousarray(factors.val, dtype=np.float64)
+    dv.download_f64(factors.val, d.val, n_out)
     return bad
 
 
@@ -41,15 +47,12 @@ def factor_serial(factors: IluFactors) -> None:
     """Up-looking ILU over all rows, in place; ZeroPivotError(first row).
 
     The device sweeps every row; as the reference stops at the first zero
-    pivot, rows after it are restored to their input values so the
-    observable state matches the reference's."""
+    pivot, only the rows up to it are copied back, so the observable state
+    matches the reference's."""
     if factors.n == 0:
         return
-    before = factors.val.copy()
-    bad = _run(factors)
+    bad = _run(factors, keep_after_bad=True)
     if bad >= 0:
-        cut = int(factors.pattern.row_start[bad + 1])
-        factors.val[cut:] = before[cut:]
         raise ZeroPivotError(int(bad))
 
 

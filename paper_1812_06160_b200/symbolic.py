@@ -78,7 +78,7 @@ class IluFactors:
     def upload_values(self) -> dv.DevIlu:
         d = self.device()
         if self.pattern.nnz:
-            d.val.copy_(dv.f64(self.val))
+            dv.upload_f64(d.val, self.val)
         return d
 
 

@@ -287,3 +287,16 @@ def config_matrix(cfg: str, scale: float = 1.0, rmat_count: int = 64):
     else:
         raise KeyError(cfg)
     return a, base, s
+
+
+def box_regions(dims, perm, parts):
+    """Grid-aligned box decomposition of a box grid, in the numbering of a
+    permuted matrix (perm: new -> natural index).  parts = boxes per axis.
+    The application-side domain decomposition a PDE code would supply."""
+    dims = tuple(int(d) for d in dims)
+    nat = np.asarray(perm, dtype=np.int64)
+    coords = np.unravel_index(nat, dims)
+    rid = np.zeros(nat.size, dtype=np.int64)
+    for a, (d, p) in enumerate(zip(dims, parts)):
+        rid = rid * p + (coords[a] * p) // d
+    return rid.astype(np.int32)
