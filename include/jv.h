@@ -163,7 +163,8 @@ int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col, double* v
               const int32_t* diag_pos, const double* norms, double tau, int milu,
               const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
               int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
-              int32_t* ticket, void* stream);
+              int32_t* ticket, const int8_t* heavy, const int64_t* elim_ptr,
+              const int32_t* elim, void* stream);
 /* `ready_below`: rows with index < ready_below were factored by an earlier
  * call (the upper stage before the lower-tail call, lower.py:273-318) and are
  * read from val directly instead of the mailbox. */
@@ -189,6 +190,21 @@ int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,
  * batch_ptr sized >= n/32 + nlev + 1; *nbatch_h returned (synchronises). */
 int jv_build_batches(int32_t nlev, const int32_t* level_ptr, int32_t* batch_ptr,
                      int32_t* nbatch_h, void* stream);
+/* Elimination lists for heavy rows (setup, once per pattern): a row is
+ * heavy when its pivots' structural candidate count
+ * sum_k min(|U(c_k)|, entries after k) exceeds min_cand (MILU: sum |U(c_k)|).
+ * heavy[n] (int8) flags them; elim_ptr[nnz+1] gives each strict-lower
+ * entry p of a heavy row its ops [elim_ptr[p], elim_ptr[p+1]) (0-length for
+ * every other entry); elim[2*nops] holds (q, w) pairs: q = index of the U
+ * entry of the pivot row that matches, w = target position in the row
+ * (MILU: w = diag offset | 1<<30 for an out-of-pattern q), ascending.  Call
+ * with elim = NULL to get *nops_h (synchronises), then again to fill.
+ * jv_factor takes (heavy, elim_ptr, elim) or three NULLs.  The lists are
+ * exactly the matches _factor_row (_kernels.py:165-194) finds by search.  */
+int jv_elim_lists(int32_t n, const int32_t* row_start, const int32_t* col,
+                  const int32_t* diag_pos, int milu, int64_t min_cand, int8_t* heavy,
+                  int64_t* elim_ptr, int32_t* elim, int64_t* nops_h, void* stream);
+
 /* Class-aware schedule used by jv_factor / jv_solve: rows (nullable = 0..m-1)
  * stably sorted by key = 2*level + class; class-0 rows of a level go 32 to a
  * batch (thread path), class-1 rows one per batch (warp path).

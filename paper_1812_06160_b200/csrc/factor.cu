@@ -62,6 +62,9 @@ struct FactorArgs {
   uint32_t epoch;
   int32_t* err;
   int* ticket;
+  const int8_t* heavy;        // nullable: rows with an elimination list
+  const int64_t* elim_ptr;    // [nnz+1]: ops of L entry p = [elim_ptr[p], elim_ptr[p+1])
+  const int2* elim;           // op = (q: U entry of the pivot row, w: target position | kOut)
 };
 
 struct WarpArena {
@@ -122,26 +125,31 @@ constexpr size_t kArenaBytes = sizeof(WarpArena) * kFactorWarps;
 
 extern __shared__ __align__(16) unsigned char jv_factor_smem[];
 
-// Per-thread slice of the shared slab: slot-major, one column per thread.
-// Addressed through the kernel's extern __shared__ array so every access
-// compiles to LDS/STS.
+// Per-thread slice of the shared slab: warp-major blocks (warp w owns a
+// contiguous 32-lane x slots block, so an idle warp can reuse its block as
+// plain scratch — the heavy-row ring), slot-major inside a block, one column
+// per lane.  Addressed through the kernel's extern __shared__ array so every
+// access compiles to LDS/STS.
+JV_INLINE int* slice_ints(int warp) {
+  return reinterpret_cast<int*>(jv_factor_smem + kArenaBytes + (size_t)kThreads * kSlotsD * 8) +
+         warp * (32 * kSlotsI);
+}
+JV_INLINE double* slice_doubles(int warp) {
+  return reinterpret_cast<double*>(jv_factor_smem + kArenaBytes) + warp * (32 * kSlotsD);
+}
 struct Slice {
   int tid;
-  JV_INLINE int* ib() const {
-    return reinterpret_cast<int*>(jv_factor_smem + kArenaBytes + (size_t)kThreads * kSlotsD * 8);
-  }
-  JV_INLINE double* db() const {
-    return reinterpret_cast<double*>(jv_factor_smem + kArenaBytes);
-  }
-  JV_INLINE int& cj(int k) const { return ib()[k * kThreads + tid]; }
-  JV_INLINE int& dq(int k) const { return ib()[(kR + k) * kThreads + tid]; }
-  JV_INLINE int& ul(int k) const { return ib()[(kR + kP + k) * kThreads + tid]; }
+  JV_INLINE int* ib() const { return slice_ints(tid >> 5) + (tid & 31); }
+  JV_INLINE double* db() const { return slice_doubles(tid >> 5) + (tid & 31); }
+  JV_INLINE int& cj(int k) const { return ib()[k * 32]; }
+  JV_INLINE int& dq(int k) const { return ib()[(kR + k) * 32]; }
+  JV_INLINE int& ul(int k) const { return ib()[(kR + kP + k) * 32]; }
   // update op o: (k << 16) | (t << 8) | target entry
-  JV_INLINE int& op(int o) const { return ib()[(kR + 2 * kP + o) * kThreads + tid]; }
-  JV_INLINE double& a(int k) const { return db()[k * kThreads + tid]; }
-  JV_INLINE double& dv(int k) const { return db()[(kR + k) * kThreads + tid]; }
-  JV_INLINE double& uv(int k, int t) const { return db()[(kR + kP + k * kU + t) * kThreads + tid]; }
-  JV_INLINE double& ls(int k) const { return db()[(kR + kP + kP * kU + k) * kThreads + tid]; }
+  JV_INLINE int& op(int o) const { return ib()[(kR + 2 * kP + o) * 32]; }
+  JV_INLINE double& a(int k) const { return db()[k * 32]; }
+  JV_INLINE double& dv(int k) const { return db()[(kR + k) * 32]; }
+  JV_INLINE double& uv(int k, int t) const { return db()[(kR + kP + k * kU + t) * 32]; }
+  JV_INLINE double& ls(int k) const { return db()[(kR + kP + kP * kU + k) * 32]; }
 };
 
 struct ShortRow {
@@ -741,8 +749,317 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
   __syncwarp();
 }
 
-constexpr size_t kFactorSmem =
-    sizeof(WarpArena) * kFactorWarps + (size_t)kThreads * (kSlotsI * 4 + kSlotsD * 8);
+// Heavy rows (power-law hubs: thousands of pivots whose U rows hold
+// thousands of entries) use the elimination list built once per pattern by
+// jv_elim_lists — the structural matches (q, w) of every pivot, in ascending
+// column order — so the numeric pass does no searching.  The row is then a
+// chain of nL steps (one division, a parallel scatter of the pivot's
+// updates); everything that does not depend on the chain is streamed ahead:
+//  * the op pairs and the mailbox packets of the pivots' U entries flow
+//    through a 512-entry per-warp ring in shared memory (the warp's idle
+//    thread-path slices), filled by cp.async five windows (64 ops each)
+//    ahead for the ops and three ahead for the packets;
+//  * the row's values live in a CTA-wide shared buffer (one heavy row per
+//    CTA at a time, try-lock; rows that do not fit or find it taken stay in
+//    HBM), so the per-step read-modify-writes are shared-memory latency.
+constexpr int kRing = 512;          // ops per warp ring
+constexpr int kWin = 64;            // ops per window (2 per lane)
+constexpr int kHeavyCap = 10752;    // row entries in the CTA heavy buffer
+constexpr size_t kSliceBytes = (size_t)kThreads * (kSlotsI * 4 + kSlotsD * 8);
+static_assert(kSlotsI * 32 >= 2 * kRing && kSlotsD * 32 >= 2 * kRing, "ring must fit the slices");
+
+JV_INLINE unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+JV_INLINE void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+JV_INLINE void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+JV_INLINE void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+JV_INLINE void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct Ring {
+  int2* ops;        // kRing (q, w) pairs
+  uint64_t* pkts;   // kRing mailbox packets (2 words each)
+  JV_INLINE int2* op(int e) const { return ops + (e & (kRing - 1)); }
+  JV_INLINE uint64_t* pkt(int e) const { return pkts + 2 * (e & (kRing - 1)); }
+};
+
+struct HeavyStream {
+  const int2* elim;
+  const uint64_t* mbox;
+  Ring R;
+  long long O0;   // first op of the row
+  int nops;       // ops of the row
+  int lane;
+  // window i: this lane's entries i*kWin + lane + {0, 32}
+  JV_INLINE void issue_ops(int i) const {
+#pragma unroll
+    for (int h = 0; h < kWin; h += 32) {
+      const int e = i * kWin + h + lane;
+      if (e < nops) cp_async8(R.op(e), elim + O0 + e);
+    }
+    cp_commit();
+  }
+  JV_INLINE void issue_pkts(int i) const {
+#pragma unroll
+    for (int h = 0; h < kWin; h += 32) {
+      const int e = i * kWin + h + lane;
+      if (e < nops) cp_async16(R.pkt(e), mbox + 2 * (long long)R.op(e)->x);
+    }
+    cp_commit();
+  }
+  JV_INLINE void prologue() const {
+    for (int i = 0; i < 5; ++i) issue_ops(i);
+    cp_wait<0>();
+    for (int i = 0; i < 3; ++i) issue_pkts(i);
+    cp_wait<0>();
+    __syncwarp();
+  }
+  // entering window i: its packets landed; windows i+5 (ops) / i+3 (packets) go out
+  JV_INLINE void advance(int i) const {
+    cp_wait<4>();
+    __syncwarp();
+    issue_ops(i + 5);
+    cp_wait<4>();
+    issue_pkts(i + 3);
+  }
+};
+
+#ifdef JV_HEAVY_PROFILE
+#define HP_T0(v) long long v = clock64()
+#define HP_ADD(acc, v) acc += clock64() - v
+#else
+#define HP_T0(v)
+#define HP_ADD(acc, v)
+#endif
+
+// u value of ring entry e (pivot row c); false when its packet is stale
+JV_INLINE bool ring_value(const FactorArgs& A, const Ring& R, int e, int c, double& u) {
+  if (c < A.ready_below) {
+    u = __ldcg(A.val + R.op(e)->x);
+    return true;
+  }
+  const uint64_t* pk = R.pkt(e);
+  const Probe p{pk[0], pk[1]};
+  if (!probe_ok(p, A.epoch)) return false;
+  u = probe_val(p);
+  return true;
+}
+
+constexpr int kGroup = 4;   // ops per lane per step (128 per warp)
+
+JV_INLINE void heavy_row(const FactorArgs& A, int r, int lane, int* heavy_busy, double* hbuf,
+                         const jv::Trace& T, int bt) {
+  [[maybe_unused]] long long hp_adv = 0, hp_miss = 0, hp_div = 0, hp_piv = 0;
+  HP_T0(hp_start);
+  const unsigned full = 0xffffffffu;
+  const int rs = A.row_start[r], re = A.row_start[r + 1];
+  const int len = re - rs;
+  const int nL = A.diag[r] - rs;
+  const double thresh = A.tau > 0.0 ? jv::dmul(A.tau, A.norms[r]) : 0.0;
+  const int wi = threadIdx.x >> 5;
+
+  // row values: a slot of the CTA buffer (two halves; a long row takes both)
+  int bits = 0;
+  if (lane == 0 && len <= kHeavyCap) {
+    for (int tries = 0; tries < 4 && !bits; ++tries) {
+      const int st = *reinterpret_cast<volatile int*>(heavy_busy);
+      int want = 0;
+      if (len > kHeavyCap / 2) want = st == 0 ? 3 : 0;
+      else if (!(st & 1)) want = 1;
+      else if (!(st & 2)) want = 2;
+      if (!want) break;
+      if (atomicCAS(heavy_busy, st, st | want) == st) bits = want;
+    }
+  }
+  bits = __shfl_sync(full, bits, 0);
+  double* av = A.val + rs;
+  if (bits) {
+    av = hbuf + (bits == 2 ? kHeavyCap / 2 : 0);
+    for (int i = lane; i < len; i += 32) av[i] = __ldcg(A.val + rs + i);
+    __syncwarp();
+  }
+
+  HeavyStream H;
+  H.elim = A.elim;
+  H.mbox = A.mbox;
+  H.R.ops = reinterpret_cast<int2*>(slice_ints(wi));
+  H.R.pkts = reinterpret_cast<uint64_t*>(slice_doubles(wi));
+  H.O0 = A.elim_ptr[rs];
+  H.nops = (int)(A.elim_ptr[rs + nL] - H.O0);
+  H.lane = lane;
+  H.prologue();
+  int cur = 0;
+  H.advance(0);
+  HP_ADD(hp_adv, hp_start);
+
+  for (int k0 = 0; k0 < nL; k0 += 32) {
+    const int kc = min(32, nL - k0);
+    int c = 0, d = 0, e1 = 0;
+    double dval = 0.0;
+    int dready = 0;
+    if (lane < kc) {
+      c = A.col[rs + k0 + lane];
+      d = A.diag[c];
+      e1 = (int)(A.elim_ptr[rs + k0 + lane + 1] - H.O0);
+      if (c < A.ready_below) {
+        dval = __ldcg(A.val + d);
+        dready = 1;
+      } else {
+        const Probe p = probe_issue(A.mbox, d);
+        if (probe_ok(p, A.epoch)) { dval = probe_val(p); dready = 1; }
+      }
+    }
+    int e0 = (int)(A.elim_ptr[rs + k0] - H.O0);
+    for (int kk = 0; kk < kc; ++kk) {
+      const int k = k0 + kk;
+      const int ck = __shfl_sync(full, c, kk);
+      const int r1 = __shfl_sync(full, e1, kk);
+      const int r0 = e0;
+      e0 = r1;
+      double piv = __shfl_sync(full, dval, kk);
+      HP_T0(t_piv);
+      if (!__shfl_sync(full, dready, kk))
+        piv = __shfl_sync(full, warp_value(A, lane == 0, ck, __shfl_sync(full, d, kk)), 0);
+      HP_ADD(hp_piv, t_piv);
+
+      if (A.milu) {
+        // MILU: the diagonal accumulates in op order — lane 0 folds each
+        // block of 32 in order (correctness path; no power-law MILU config)
+        double l = 0.0;
+        int drop = 0;
+        if (lane == 0) {
+          l = jv::ddiv(av[k], piv);
+          drop = A.tau > 0.0 && fabs(l) < thresh;
+          av[k] = drop ? 0.0 : l;
+        }
+        l = __shfl_sync(full, l, 0);
+        drop = __shfl_sync(full, drop, 0);
+        for (int b = r0; b < r1; b += 32) {
+          const int need = (min(b + 32, r1) - 1) / kWin;
+          while (cur < need) H.advance(++cur);
+          const int e = b + lane;
+          double u = 0.0;
+          int w = 0;
+          bool miss = false;
+          if (e < r1) {
+            w = H.R.op(e)->y;
+            miss = !ring_value(A, H.R, e, ck, u);
+          }
+          if (__any_sync(full, miss)) {
+            const double v = warp_value(A, miss, ck, miss ? H.R.op(e)->x : 0);
+            if (miss) u = v;
+          }
+          const double prod = jv::dmul(l, u);
+          const int wt0 = (drop || (w & kOut)) ? nL : w;
+          for (int t = 0; t < 32 && b + t < r1; ++t) {
+            const double pt = __shfl_sync(full, prod, t);
+            const int wt = __shfl_sync(full, wt0, t);
+            if (lane == 0) av[wt] = jv::dsub(av[wt], pt);
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+
+      // groups of up to 32 * kGroup ops: the loads of a group (op, packet,
+      // target value) are issued together, before the division they do not
+      // depend on; every lane computes l itself (no broadcast)
+      HP_T0(t_div);
+      const bool direct = ck < A.ready_below;
+      double l = 0.0;
+      bool drop = false;
+      for (int g0 = r0;; g0 += 32 * kGroup) {
+        const int gend = min(g0 + 32 * kGroup, r1);
+        if (g0 < gend) {
+          HP_T0(t_adv);
+          const int need = (gend - 1) / kWin;
+          while (cur < need) H.advance(++cur);
+          HP_ADD(hp_adv, t_adv);
+        }
+        int w[kGroup];
+        double u[kGroup], tv[kGroup];
+        unsigned missm = 0;
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          const int e = g0 + 32 * j + lane;
+          w[j] = -1;
+          u[j] = 0.0;
+          tv[j] = 0.0;
+          if (e < gend) {
+            const int2 op = *H.R.op(e);
+            w[j] = op.y;
+            if (direct) {
+              u[j] = __ldcg(A.val + op.x);
+            } else {
+              const ulonglong2 pk = *reinterpret_cast<const ulonglong2*>(H.R.pkt(e));
+              u[j] = __longlong_as_double((long long)((pk.x & 0xffffffffull) | (pk.y << 32)));
+              if ((uint32_t)(pk.x >> 32) != A.epoch || (uint32_t)(pk.y >> 32) != A.epoch)
+                missm |= 1u << j;
+            }
+            tv[j] = av[op.y];
+          }
+        }
+        if (g0 == r0) {
+          const double a = av[k];
+          bool slow;
+          l = jv::ddiv_fast(a, piv, slow);
+          if (slow) l = __ddiv_rn(a, piv);
+          drop = A.tau > 0.0 && fabs(l) < thresh;
+          if (lane == 0) av[k] = drop ? 0.0 : l;
+          HP_ADD(hp_div, t_div);
+        }
+        if (g0 >= gend || drop) break;
+        if (__any_sync(full, missm != 0)) {
+          HP_T0(t_miss);
+#pragma unroll
+          for (int j = 0; j < kGroup; ++j) {
+            const int e = g0 + 32 * j + lane;
+            const bool m = (missm >> j) & 1;
+            const double v = warp_value(A, m, ck, m ? H.R.op(e)->x : 0);
+            if (m) u[j] = v;
+          }
+          HP_ADD(hp_miss, t_miss);
+        }
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j)
+          if (w[j] >= 0) av[w[j]] = jv::dsub(tv[j], jv::dmul(l, u[j]));
+        if (gend >= r1) break;
+      }
+      __syncwarp();
+    }
+  }
+  cp_wait<0>();
+  __syncwarp();
+  // ---- publish
+  for (int i = lane; i < len; i += 32) {
+    const double v = av[i];
+    if (bits) __stcg(A.val + rs + i, v);
+    if (i >= nL) jv::mbox_put(A.mbox, rs + i, v, A.epoch);
+  }
+  if (lane == 0 && av[nL] == 0.0) atomicMin(A.err, r);
+  __syncwarp();
+  if (bits && lane == 0) atomicAnd(heavy_busy, ~bits);
+  __syncwarp();
+#ifdef JV_HEAVY_PROFILE
+  if (lane == 0) {
+    // words 7, 13-15 (the batch marks use 0-6 and 8-12)
+    jv::trace_word(T, bt, 7, ((unsigned long long)hp_piv << 1) | (bits != 0));
+    jv::trace_word(T, bt, 13, hp_adv);
+    jv::trace_word(T, bt, 14, hp_miss);
+    jv::trace_word(T, bt, 15, ((unsigned long long)hp_div << 32) | (unsigned)(clock64() - hp_start));
+  }
+#else
+  (void)T; (void)bt; (void)hp_adv; (void)hp_miss; (void)hp_div; (void)hp_piv;
+#endif
+}
+
+constexpr size_t kFactorSmem = kArenaBytes + kSliceBytes + sizeof(double) * kHeavyCap;
+static_assert(kFactorSmem <= 232448 - 64, "factor kernel shared memory");
 
 __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
   WarpArena* arena = reinterpret_cast<WarpArena*>(jv_factor_smem);
@@ -752,6 +1069,10 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
   const Slice S{(int)threadIdx.x};
   const jv::Trace T = jv::trace_begin();
   const int nw = (gridDim.x * blockDim.x) >> 5;
+  __shared__ int heavy_busy;
+  double* hbuf = reinterpret_cast<double*>(jv_factor_smem + kArenaBytes + kSliceBytes);
+  if (threadIdx.x == 0) heavy_busy = 0;
+  __syncthreads();
   for (;;) {
     const int b = jv::ticket_next(A.ticket, lane, T);
     if (b >= A.nbatch) break;
@@ -788,7 +1109,9 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
-      warp_row(A, __shfl_sync(full, r, src), lane, W);
+      const int rr = __shfl_sync(full, r, src);
+      if (A.heavy != nullptr && A.heavy[rr]) heavy_row(A, rr, lane, &heavy_busy, hbuf, T, b);
+      else warp_row(A, rr, lane, W);
     }
     __syncwarp();
     if (lane == 0) jv::trace_mark(T, b, 4);
@@ -824,14 +1147,16 @@ extern "C" int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col
                          const int32_t* diag_pos, const double* norms, double tau, int milu,
                          const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
                          int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
-                         int32_t* ticket, void* stream) {
+                         int32_t* ticket, const int8_t* heavy, const int64_t* elim_ptr,
+                         const int32_t* elim, void* stream) {
   if (n < 0 || nbatch < 0 || epoch == 0) {
     jvh::set_error("jv_factor: bad argument (n=%d nbatch=%d epoch=%u)", n, nbatch, epoch);
     return JV_EINVAL;
   }
   if (n == 0 || nbatch == 0) return JV_OK;
   FactorArgs A{row_start, col, val, diag_pos, norms, tau, milu, order, batch_ptr,
-               nbatch, ready_below, mbox, epoch, err_row, ticket};
+               nbatch, ready_below, mbox, epoch, err_row, ticket,
+               elim != nullptr ? heavy : nullptr, elim_ptr, reinterpret_cast<const int2*>(elim)};
   void* args[] = {&A};
   return jvh::persistent_launch(factor_kernel, kThreads, args, (cudaStream_t)stream, "jv_factor",
                                 kFactorSmem);

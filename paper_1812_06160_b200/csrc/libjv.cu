@@ -5,5 +5,6 @@
 #include "factor.cu"
 #include "solve.cu"
 #include "setup.cu"
+#include "elim.cu"
 #include "region.cu"
 #include "host.cpp"

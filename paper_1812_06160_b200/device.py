@@ -330,6 +330,7 @@ class DevIlu:
         self._fsched = None
         self._fsched_milu = None
         self._rplan = None
+        self._elim = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
         self.fbox = Mailbox(self.nnz, 2)
@@ -361,6 +362,28 @@ class DevIlu:
                                                           self._classes("factor"))
             self._fsched_milu = self.milu
         return self._fsched
+
+    # heavy rows: structural matches precomputed once per pattern (jv_elim_lists)
+    ELIM_MIN_CAND = 256
+
+    def elim_lists(self):
+        """(heavy, elim_ptr, elim) device buffers, or None if no row is heavy."""
+        key = bool(self.milu)
+        if self._elim is None or self._elim[0] != key:
+            t = torch()
+            heavy = t.empty(max(self.n, 1), dtype=t.int8, device="cuda")
+            eptr = t.empty(self.nnz + 1, dtype=t.int64, device="cuda")
+            nops = ctypes.c_int64(0)
+            args = [self.n, ptr(self.row_start), ptr(self.col), ptr(self.diag_pos), int(self.milu),
+                    self.ELIM_MIN_CAND, ptr(heavy), ptr(eptr)]
+            _lib.call("jv_elim_lists", *args, None, ctypes.byref(nops), stream())
+            lists = None
+            if nops.value > 0:
+                elim = t.empty(2 * nops.value, dtype=t.int32, device="cuda")
+                _lib.call("jv_elim_lists", *args, ptr(elim), ctypes.byref(nops), stream())
+                lists = (heavy, eptr, elim, int(nops.value))
+            self._elim = (key, lists)
+        return self._elim[1]
 
     def fwd_schedule(self):
         if self._fwd is None:
@@ -462,6 +485,7 @@ class DevIlu:
                       ptr(self.fbox.buf), self.fbox.next_epoch(), ptr(self.err), stream())
             return
         sched = self.factor_schedule()
+        el = self.elim_lists()
         if lo > 0 or hi < self.n:
             sched = sched.restrict(lo, hi)
         if norms:
@@ -470,7 +494,9 @@ class DevIlu:
         _lib.call("jv_factor", self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
                   ptr(self.diag_pos), ptr(self.norms), self.tau, int(self.milu), ptr(sched.order),
                   ptr(sched.batch_ptr), sched.nbatch, int(ready_below), ptr(self.fbox.buf),
-                  self.fbox.next_epoch(), ptr(self.err), ptr(self.ticket), stream())
+                  self.fbox.next_epoch(), ptr(self.err), ptr(self.ticket),
+                  ptr(el[0]) if el else None, ptr(el[1]) if el else None,
+                  ptr(el[2]) if el else None, stream())
 
     def factor(self, lo=0, hi=None, ready_below=0):
         """Factor and return the smallest zero-pivot row (or -1)."""

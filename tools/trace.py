@@ -58,7 +58,10 @@ def main():
                        (f"tridiag{args.tridiag}" if args.tridiag else args.config))
     os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
     np.savez_compressed(os.path.join(REPO, "gpurun_out", f"trace_{tag}.npz"), tr=tr, bp=bp,
-                        first=first, key=keys[first])
+                        first=first, key=keys[first],
+                        rs=dv.host_i64(ilu.row_start, ilu.n + 1), diag=dv.host_i64(ilu.diag_pos, ilu.n),
+                        heavy=(ilu.elim_lists()[0][:ilu.n].cpu().numpy() if ilu.elim_lists()
+                               else np.zeros(ilu.n, np.int8)))
     lev = keys[first] // 2
     cls = keys[first] % 2
     t = tr[:, :5] - tr[:, 0].min()
