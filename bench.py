@@ -54,12 +54,25 @@ def alg_bytes(n, nnz_a, nnz_f):
     )
 
 
-def build_config(cfg):
+def build_config(cfg, rank=0, world=1, rmat_count=64):
+    """Matrix + device plan of the config.  c5 (a batch of independent R-MAT
+    systems) is sharded: this rank builds the block-diagonal matrix of its
+    contiguous block of seeds (dist.shard_range); `blocks` lists them."""
     import paper_1812_06160_b200 as jv
     from paper_1812_06160_b200 import workloads as W
+    from paper_1812_06160_b200.dist import shard_range
     from paper_1812_06160_b200.plan import build_plan
 
-    a, base, s = W.config_matrix(cfg)
+    blocks = None
+    if cfg == "c5":
+        s = W.CONFIGS[cfg]
+        seeds = list(shard_range(rmat_count, rank, world))
+        mats = [W.rmat(18, sd) for sd in seeds]
+        blocks = [(sd, m.n) for sd, m in zip(seeds, mats)]
+        a, base = W.block_diagonal(mats), None
+        del mats
+    else:
+        a, base, s = W.config_matrix(cfg)
     if base == "rcm":
         base_perm = jv.rcm_order(a.pattern).perm
     elif base is None:
@@ -68,7 +81,15 @@ def build_config(cfg):
         base_perm = base.perm
     plan = build_plan(a, base_perm=base_perm, k=s["k"], tau=s["tau"],
                       min_level_rows=s["min_level_rows"])
-    return a, plan, s
+    return a, plan, s, blocks
+
+
+def rhs(n, blocks):
+    """b drawn in the original order (uniform[-1,1], seed 0 per system, as
+    the reference's krylov.py:199 / SURVEY.md §8d), one draw per block."""
+    if blocks is None:
+        return np.random.default_rng(0).uniform(-1.0, 1.0, n)
+    return np.concatenate([np.random.default_rng(0).uniform(-1.0, 1.0, m) for _, m in blocks])
 
 
 class ClockSampler:
@@ -123,9 +144,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(cfg, plan, seconds=12.0):
+def cpu_baseline(cfg, plan, seconds=12.0, blocks=None):
     """The reference's algorithm on the host (the pinned C oracle), serial
-    and threaded, on the same matrix; bounded to ~`seconds` of CPU work."""
+    and threaded, on the same matrix; bounded to ~`seconds` of CPU work.
+    For the c5 batch the sample is ONE system of the batch (the throughput
+    unit, nnz/s, is per-nonzero so it carries over)."""
     import oracle
     from paper_1812_06160_b200 import device as dv
 
@@ -135,12 +158,19 @@ def cpu_baseline(cfg, plan, seconds=12.0):
     col = dv.host_i64(ilu.col, ilu.nnz)
     diag = dv.host_i64(ilu.diag_pos, n)
     val = dv.host_f64(plan.assembled, ilu.nnz)
+    sample = f"full {cfg} factorization"
+    if blocks is not None:
+        from paper_1812_06160_b200 import workloads as W
+        sd = blocks[0][0]
+        fe = oracle.front_end(*(lambda m: (m.n, m.row_start, m.col, m.val))(W.rmat(18, sd)))
+        rs, col, diag, val = fe["row_start"], fe["col"], fe["diag"], fe["val"]
+        sample = f"one system of the c5 batch (R-MAT seed {sd})"
     tau = ilu.tau
     cores = os.cpu_count() or 1
     res = {}
     deadline = time.perf_counter() + seconds
     ts, tp = [], []
-    while time.perf_counter() < deadline or len(ts) < 2:
+    while time.perf_counter() < deadline or len(ts) < 1:
         t0 = time.perf_counter()
         oracle.factor_serial(rs, col, val, diag, tau)
         ts.append(time.perf_counter() - t0)
@@ -152,12 +182,129 @@ def cpu_baseline(cfg, plan, seconds=12.0):
     res["serial_s"] = statistics.median(ts)
     res["threaded_s"] = statistics.median(tp)
     res["runs"] = len(ts)
+    res["nnz"] = int(col.size)
+    res["sample"] = f"{sample}, serial + threaded p2p oracle x{len(ts)}"
     return res, cores
 
 
 def digest(a, kind):
     a = np.ascontiguousarray(a, dtype=np.int64 if kind == "i" else np.float64)
     return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def block_rows(perm, blocks):
+    """New-order rows of each block of a block-diagonal plan (c5): the level
+    permutation keeps every block's relative order, so these rows, in order,
+    are exactly that system's own factor rows."""
+    out, off = {}, 0
+    for sd, m in blocks:
+        out[sd] = np.flatnonzero((perm >= off) & (perm < off + m))
+        off += m
+    return out
+
+
+def take_rows(rs, val, rows):
+    lens = rs[rows + 1] - rs[rows]
+    starts = np.concatenate([[0], np.cumsum(lens)])[:-1]
+    idx = np.repeat(rs[rows] - starts, lens) + np.arange(int(lens.sum()))
+    return val[idx]
+
+
+def parity_check(cfg, ilu, plan, x, sy, blocks, n):
+    """Bitwise digests of the timed arrays against the reference's full-size
+    digests (tests/golden/full_digests.json); None when none apply."""
+    from paper_1812_06160_b200 import device as dv
+    dpath = os.path.join(REPO, "tests", "golden", "full_digests.json")
+    if not os.path.exists(dpath):
+        return None
+    allg = json.load(open(dpath))
+    if blocks is None:
+        d = allg.get(cfg)
+        if not d:
+            return None
+        return (digest(ilu.host_val(), "f") == d["digests"]["fval"]
+                and digest(dv.host_f64(x, n), "f") == d["digests"]["x"]
+                and digest(dv.host_f64(sy, n), "f") == d["digests"]["spmv_perm"])
+    have = [sd for sd, _ in blocks if f"c5_seed{sd}" in allg]
+    if not have:
+        return None
+    perm = dv.host_i64(plan.perm, n)
+    rows = block_rows(perm, blocks)
+    rs = dv.host_i64(ilu.row_start, n + 1)
+    val = ilu.host_val()
+    xh, syh = dv.host_f64(x, n), dv.host_f64(sy, n)
+    ok = True
+    for sd in have:
+        d = allg[f"c5_seed{sd}"]["digests"]
+        r = rows[sd]
+        ok &= digest(take_rows(rs, val, r), "f") == d["fval"]
+        ok &= digest(xh[r], "f") == d["x"]
+        # the block's spmv rows: hub rows beyond one tile are tree-summed
+        # (1e-12), so the spmv digest is informative only
+    return bool(ok)
+
+
+def measure_spmv_dist(plan, steps, world, rank):
+    """Row-partitioned spmv of the config's (permuted) matrix over all ranks
+    with one NCCL halo exchange per product (dist.DistSpmv): back-to-back
+    (Krylov-like) and single-shot device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_1812_06160_b200 import device as dv
+    from paper_1812_06160_b200 import dist as jd
+
+    A = plan.permuted
+    n = A.n
+    rs, col = A.host_pattern()
+    val = dv.host_f64(A.val, A.nnz)
+    bounds = jd.row_partition(rs, world)
+    hp = jd.plan_halo(rs, col, val, bounds, rank, world)
+    sp = jd.DistSpmv(hp)
+    x = np.random.default_rng(0).uniform(-1.0, 1.0, n)
+    sp.x_local.copy_(dv.f64(x[hp.lo:hp.hi]))
+    y = dv.empty_f64(max(hp.n_local, 1))
+    for _ in range(5):
+        sp(sp.x_local, y)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(steps):
+        sp(sp.x_local, y)
+    e1.record()
+    torch.cuda.synchronize()
+    b2b = e0.elapsed_time(e1) / steps
+    single = []
+    for _ in range(min(steps, 20)):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        sp(sp.x_local, y)
+        e1.record()
+        torch.cuda.synchronize()
+        single.append(e0.elapsed_time(e1))
+    t = torch.tensor([b2b, statistics.median(single)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    b2b, one = [float(v) for v in t.tolist()]
+    # bitwise check of the distributed product against the whole-matrix one
+    parts = [None] * world
+    dist.all_gather_object(parts, (hp.lo, dv.host_f64(y, hp.n_local)))
+    ok = None
+    if rank == 0:
+        import oracle
+        full = np.zeros(n)
+        for lo, part in parts:
+            full[lo:lo + part.size] = part
+        ok = bool(np.array_equal(full, oracle.spmv(rs, col, val, x)))
+    nbytes = alg_bytes(n, A.nnz, 0)["spmv"]
+    peak, _ = peaks()
+    return {"ranks": world, "partition": "contiguous rows, nnz-balanced",
+            "back_to_back_us": b2b * 1e3, "single_shot_us": one * 1e3,
+            "GBps_aggregate": nbytes / (b2b * 1e-3) / 1e9,
+            "frac_of_world_peak": nbytes / (b2b * 1e-3) / 1e9 / (peak * world),
+            "single_shot_GBps": nbytes / (one * 1e-3) / 1e9,
+            "halo_bytes_rank0": hp.halo_bytes, "peers_rank0": hp.stats["peers"],
+            "boundary_rows_rank0": hp.stats["boundary_rows"], "bitwise_vs_oracle": ok}
 
 
 def run_mine(args):
@@ -173,16 +320,18 @@ def run_mine(args):
 
     from paper_1812_06160_b200 import device as dv
 
-    a, plan, s = build_config(args.config)
+    a, plan, s, blocks = build_config(args.config, rank, world, args.rmat_count)
+    batched = blocks is not None
     ilu = plan.ilu
     n, nnz_f, nnz_a = ilu.n, ilu.nnz, plan.permuted.nnz
     ab = alg_bytes(n, nnz_a, nnz_f)
     perm = dv.host_i64(plan.perm, n)
-    b = dv.f64(np.random.default_rng(0).uniform(-1.0, 1.0, n)[perm])
+    b = dv.f64(rhs(n, blocks)[perm])
     y = dv.empty_f64(n)
     x = dv.empty_f64(n)
     sy = dv.empty_f64(n)
     ilu.factor_schedule()
+    ilu.elim_lists()
     ilu.fwd_schedule()
     ilu.bwd_schedule()
     plan.permuted.tile_rows()
@@ -235,28 +384,37 @@ def run_mine(args):
     fw_ms = [e[1].elapsed_time(e[2]) for e in evs]
     bw_ms = [e[2].elapsed_time(e[3]) for e in evs]
     sp_ms = [e[3].elapsed_time(e[4]) for e in evs]
+    mine = torch.tensor([float(nnz_f), float(nnz_a), float(n)], dtype=torch.float64, device="cuda")
     times = torch.tensor([total_ms, sum(f_ms), sum(fw_ms) + sum(bw_ms), sum(sp_ms)],
                          dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
+        dist.all_reduce(mine, op=dist.ReduceOp.SUM)
     total_ms, f_sum, st_sum, sp_sum = [float(v) for v in times.tolist()]
+    tot_nnz_f, tot_nnz_a, tot_n = [int(v) for v in mine.tolist()]
     K = args.steps
     f_avg, st_avg, sp_avg = f_sum / K / 1e3, st_sum / K / 1e3, sp_sum / K / 1e3   # seconds
 
-    # parity of the timed arrays against the reference's full-size digests
-    parity = None
-    dpath = os.path.join(REPO, "tests", "golden", "full_digests.json")
-    if os.path.exists(dpath):
-        d = json.load(open(dpath)).get(args.config)
-        if d:
-            parity = (digest(ilu.host_val(), "f") == d["digests"]["fval"]
-                      and digest(dv.host_f64(x, n), "f") == d["digests"]["x"]
-                      and digest(dv.host_f64(sy, n), "f") == d["digests"]["spmv_perm"])
+    parity = parity_check(args.config, ilu, plan, x, sy, blocks, n)
+    if world > 1:
+        pl = [None] * world
+        dist.all_gather_object(pl, parity)
+        parity = None if all(p is None for p in pl) else all(p in (None, True) for p in pl)
 
     # end to end through the public API (host numpy buffers in, out)
     e2e = measure_e2e(a, plan, args)
+    if world > 1:
+        et = torch.tensor([e2e["ms"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e["ms"] = float(et.item())
+        e2e["value"] = (tot_nnz_f if batched else world * nnz_f) / (e2e["ms"] / 1e3)
+
+    multi = None
+    if world > 1 and not batched:
+        multi = {"spmv_dist": measure_spmv_dist(plan, max(K, 20), world, rank)}
 
     peak, peak_kind = peaks()
+    # per-GPU algorithmic bytes (every rank factors its own matrix / shard)
     ach = ab["factor"] / f_avg / 1e9
     prof = load_profile(args.config)
     paths = {
@@ -268,22 +426,32 @@ def run_mine(args):
         "spmv": {"us": sp_avg * 1e6, "alg_bytes": ab["spmv"], "GBps": ab["spmv"] / sp_avg / 1e9,
                  "frac": ab["spmv"] / sp_avg / 1e9 / peak},
     }
+    if batched:
+        workload = f"c5:rmat18_x{args.rmat_count} (block-diagonal shard per rank)"
+        value = tot_nnz_f / f_avg
+        scaling = "strong"
+        par = f"batch-sharded dp{world} ({len(blocks)} systems on rank {rank})"
+    else:
+        workload = f"{args.config}:{s['name']}"
+        value = world * nnz_f / f_avg
+        scaling = "weak"
+        par = f"replicas{world}" + (" + row-partitioned spmv" if world > 1 else "")
     line = {
         "metric": "ILU factor nnz/s, stri and spmv GB/s (fp64) vs HBM roofline; 1/2/4/8 GPU",
-        "value": world * nnz_f / f_avg,
+        "value": value,
         "unit": "factor nnz/s",
         "n_gpus": world,
         "steps": K,
         "warmup": args.warmup,
         "ms_per_step": total_ms / K,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY.md §8d recipe)",
-        "config": {"workload": f"{args.config}:{s['name']}", "n": n, "nnz_a": nnz_a,
-                   "nnz_f": nnz_f, "k": s["k"], "tau": s["tau"], "levels": plan.nlev,
-                   "n_upper": plan.n_upper, "parallelism": f"replicas{world}",
+        "config": {"workload": workload, "n": n, "nnz_a": nnz_a, "nnz_f": nnz_f,
+                   "total_nnz_f": tot_nnz_f, "k": s["k"], "tau": s["tau"], "levels": plan.nlev,
+                   "n_upper": plan.n_upper, "parallelism": par,
                    "l2": "inputs > 126 MB L2, no flush needed"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak, "peak_kind": peak_kind,
@@ -296,13 +464,14 @@ def run_mine(args):
         "parity_vs_reference": parity,
         "zero_pivot_row": bad,
     }
+    if multi:
+        line["multi_gpu"] = multi
     if world == 1 and rank == 0 and not args.no_cpu:
-        cb, cores = cpu_baseline(args.config, plan, seconds=args.cpu_seconds)
+        cb, cores = cpu_baseline(args.config, plan, seconds=args.cpu_seconds, blocks=blocks)
         line["cpu_baseline"] = {
-            "value": nnz_f / cb["threaded_s"], "unit": "factor nnz/s", "cores": cores,
-            "kind": "port",
-            "sample": f"full {args.config} factorization, threaded p2p oracle x{cb['runs']}",
-            "serial_value": nnz_f / cb["serial_s"], "serial_cores": 1,
+            "value": cb["nnz"] / cb["threaded_s"], "unit": "factor nnz/s", "cores": cores,
+            "kind": "port", "sample": cb["sample"],
+            "serial_value": cb["nnz"] / cb["serial_s"], "serial_cores": 1,
         }
     if rank == 0:
         print(json.dumps(line))
@@ -357,7 +526,12 @@ def run_reference(args):
     from paper_1812_06160_b200 import workloads as W
     from oracle import front_end
 
-    a, base, s = W.config_matrix(args.config)
+    if args.config == "c5":
+        # one system of the batch per step (nnz/s is per nonzero, the
+        # systems are independent): the bounded sample of the workload
+        a, base, s = W.rmat(18, 0), None, W.CONFIGS["c5"]
+    else:
+        a, base, s = W.config_matrix(args.config)
     if base == "rcm":
         sym_rs, sym_col = oracle.symmetrize(a.n, a.row_start, a.col)
         base_perm = oracle.rcm(sym_rs, sym_col)
@@ -388,8 +562,9 @@ def run_reference(args):
         "data": "synthetic (seeded generator, SURVEY.md §8d recipe)",
         "config": {"workload": f"{args.config}:{s['name']}", "n": a.n, "nnz_f": nnz_f},
         "cpu_baseline": {"value": v, "unit": "factor nnz/s", "cores": cores, "kind": "port",
-                         "sample": f"full {args.config} factorization per step, threaded p2p "
-                                   f"restatement of factor_p2p_kernel"},
+                         "sample": (f"one R-MAT system of the c5 batch per step" if args.config == "c5"
+                                    else f"full {args.config} factorization per step") +
+                                   ", threaded p2p restatement of factor_p2p_kernel"},
         "e2e": {"value": v, "unit": "factor nnz/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))
@@ -404,6 +579,7 @@ def main():
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--rmat-count", type=int, default=64, help="c5 batch size")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

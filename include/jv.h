@@ -80,6 +80,13 @@ int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, int32_t* tile
 int jv_spmv(int32_t n, int32_t nnz, const int32_t* row_start, const int32_t* col,
             const double* val, const double* x, double* y, const int32_t* tile_rows,
             void* stream);
+/* Row-mapped variant for the multi-GPU interior/boundary split: CSR row r is
+ * written to y[row_map[r]] (row_map nullable = identity).                  */
+int jv_spmv_rows(int32_t n, int32_t nnz, const int32_t* row_start, const int32_t* col,
+                 const double* val, const double* x, double* y, const int32_t* tile_rows,
+                 const int32_t* row_map, void* stream);
+/* dst[i] = src[idx[i]], i < n — packs the halo entries a peer needs.      */
+int jv_gather(int32_t n, const int32_t* idx, const double* src, double* dst, void* stream);
 /* Batches of independent systems (config 5) are stored as ONE
  * block-diagonal CSR (column indices offset by each block's first row), so
  * every entry point below serves them unchanged and the level schedule of

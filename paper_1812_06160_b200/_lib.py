@@ -36,6 +36,8 @@ _SIGS = {
     "jv_spmv_tile": [],
     "jv_spmv_plan": [c_int32, c_int32, _P, _P, _P],
     "jv_spmv": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P],
+    "jv_spmv_rows": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P],
+    "jv_gather": [c_int32, _P, _P, _P, _P],
     "jv_levels": [c_int, c_int32, _P, _P, _P, _P, c_uint32, _I32P, _P],
     "jv_level_sort": [c_int32, c_int32, _P, _P, _P, _P],
     "jv_partition": [c_int32, c_int32, _P, _P, _P, c_int32, c_double, c_int, _I32P, _I32P, _P],

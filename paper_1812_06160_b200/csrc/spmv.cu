@@ -45,7 +45,7 @@ __global__ void spmv_plan_kernel(int n, int nnz, int ntiles, const int32_t* rs, 
 __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
     int n, int nnz, const int32_t* __restrict__ rs, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-    const int32_t* __restrict__ tile_rows) {
+    const int32_t* __restrict__ tile_rows, const int32_t* __restrict__ row_map) {
   __shared__ double prod[kBuf];
   __shared__ double red[kSpmvThreads / 32];
   const int t = blockIdx.x;
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
     const int a = __ldg(rs + r) - p0, b = __ldg(rs + r + 1) - p0;
     double s = 0.0;
     for (int q = a; q < b; ++q) s = jv::dadd(s, prod[q]);
-    __stcs(y + r, s);
+    __stcs(y + (row_map ? __ldg(row_map + r) : r), s);
   }
   if (rlast == r1) return;
   // long row: strided partial sums, warp tree, then the 8 warp sums in order
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
   if (threadIdx.x == 0) {
     double tot = 0.0;
     for (int w = 0; w < kSpmvThreads / 32; ++w) tot = jv::dadd(tot, red[w]);
-    y[rlast] = tot;
+    y[row_map ? row_map[rlast] : rlast] = tot;
   }
 }
 
@@ -112,7 +112,39 @@ extern "C" int jv_spmv(int32_t n, int32_t nnz, const int32_t* row_start, const i
   if (n == 0) return JV_OK;
   const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
   spmv_stream_kernel<<<ntiles, kSpmvThreads, 0, (cudaStream_t)stream>>>(n, nnz, row_start, col,
-                                                                        val, x, y, tile_rows);
+                                                                        val, x, y, tile_rows,
+                                                                        nullptr);
   JV_CHECK_LAUNCH("jv_spmv");
+  return JV_OK;
+}
+
+extern "C" int jv_spmv_rows(int32_t n, int32_t nnz, const int32_t* row_start, const int32_t* col,
+                            const double* val, const double* x, double* y,
+                            const int32_t* tile_rows, const int32_t* row_map, void* stream) {
+  if (n < 0 || nnz < 0) { jvh::set_error("jv_spmv_rows: bad size"); return JV_EINVAL; }
+  if (n == 0) return JV_OK;
+  const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
+  spmv_stream_kernel<<<ntiles, kSpmvThreads, 0, (cudaStream_t)stream>>>(n, nnz, row_start, col,
+                                                                        val, x, y, tile_rows,
+                                                                        row_map);
+  JV_CHECK_LAUNCH("jv_spmv_rows");
+  return JV_OK;
+}
+
+namespace {
+__global__ void gather_f64_kernel(int n, const int32_t* __restrict__ idx,
+                                  const double* __restrict__ src, double* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = __ldg(src + __ldg(idx + i));
+}
+}  // namespace
+
+extern "C" int jv_gather(int32_t n, const int32_t* idx, const double* src, double* dst,
+                         void* stream) {
+  if (n < 0) { jvh::set_error("jv_gather: bad size"); return JV_EINVAL; }
+  if (n == 0) return JV_OK;
+  const int grid = min((n + 255) / 256, 148 * 8);
+  gather_f64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
+  JV_CHECK_LAUNCH("jv_gather");
   return JV_OK;
 }

@@ -1,4 +1,3 @@
-rm -f paper_1812_06160_b200/libjv.so
-JV_NVCC_EXTRA=-DJV_HEAVY_PROFILE python -c "import __graft_entry__ as g; g.build()" || exit 1
-for a in "5000 73" "5000 8" "5000 1"; do JV_TRACE=1 timeout 300 python tools/heavy_bench.py $a 2>&1 | tail -1; done
-rm -f paper_1812_06160_b200/libjv.so
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 600 python -m pytest tests/test_gpu_dist.py -q -x 2>&1 | tail -2
+timeout 900 python bench.py --config c5 --rmat-count 4 --steps 3 --warmup 3 --cpu-seconds 5 2>&1 | tail -3
