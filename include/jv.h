@@ -61,6 +61,13 @@ int jv_set_spin_limit(unsigned limit);
  * sync-free kernels use before touching their own mailbox packets
  * (default 64; 0 = busy poll). */
 int jv_set_backoff(unsigned cap_ns);
+/* which sync-free kernels wait at that gate (bit 0: factor, bit 1: forward
+ * and backward solves; default 0: measured faster on configs 1, 2, 4).
+ * Without it the converged probe loops wait on every needed packet
+ * directly, with their own backoff capped at jv_set_poll (default 32 ns,
+ * min 16). */
+int jv_set_gate(unsigned mask);
+int jv_set_poll(unsigned cap_ns);
 /* diagnostics: record 4 globaltimer stamps per factor batch into buf
  * (device, 16*batches uint64; NULL disables) */
 int jv_set_trace(unsigned long long* buf, long long batches);
@@ -197,20 +204,27 @@ int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,
  * batch_ptr sized >= n/32 + nlev + 1; *nbatch_h returned (synchronises). */
 int jv_build_batches(int32_t nlev, const int32_t* level_ptr, int32_t* batch_ptr,
                      int32_t* nbatch_h, void* stream);
-/* Elimination lists for heavy rows (setup, once per pattern): a row is
- * heavy when its pivots' structural candidate count
- * sum_k min(|U(c_k)|, entries after k) exceeds min_cand (MILU: sum |U(c_k)|).
- * heavy[n] (int8) flags them; elim_ptr[nnz+1] gives each strict-lower
- * entry p of a heavy row its ops [elim_ptr[p], elim_ptr[p+1]) (0-length for
- * every other entry); elim[2*nops] holds (q, w) pairs: q = index of the U
- * entry of the pivot row that matches, w = target position in the row
- * (MILU: w = diag offset | 1<<30 for an out-of-pattern q), ascending.  Call
- * with elim = NULL to get *nops_h (synchronises), then again to fill.
- * jv_factor takes (heavy, elim_ptr, elim) or three NULLs.  The lists are
- * exactly the matches _factor_row (_kernels.py:165-194) finds by search.  */
+/* Elimination lists (setup, once per pattern): the structural matches of
+ * every pivot of a row — what _factor_row (_kernels.py:165-194) finds by
+ * search — precomputed so the numeric kernel does no searching.
+ * Rows with pivots get a list when their candidate count
+ * sum_k min(|U(c_k)|, entries after k) exceeds min_cand (MILU: sum |U(c_k)|)
+ * or, with cls (nullable: jv_classify_factor classes), when they are
+ * warp-path rows.  A listed row is heavy (flag 2, the power-law path) when
+ * one of its 32-pivot chunks holds more than 256 ops (the warp op list) —
+ * or always when min_cand < 256 (diagnostic setting); otherwise flag 1 (the
+ * warp path reads its op list instead of searching).  Thread-path
+ * rows (cls 0) get none (flag 0).  heavy[n] (int8) holds the flags;
+ * elim_ptr[nnz+1] gives each strict-lower entry p of a listed row its ops
+ * [elim_ptr[p], elim_ptr[p+1]) (0-length for every other entry);
+ * elim[2*nops] holds (q, w) pairs: q = index of the matching U entry of the
+ * pivot row, w = target position in the row (MILU: w = diag offset | 1<<30
+ * for an out-of-pattern q), ascending.  Call with elim = NULL to get
+ * *nops_h (synchronises), then again to fill.  jv_factor takes (heavy,
+ * elim_ptr, elim) or three NULLs.                                          */
 int jv_elim_lists(int32_t n, const int32_t* row_start, const int32_t* col,
-                  const int32_t* diag_pos, int milu, int64_t min_cand, int8_t* heavy,
-                  int64_t* elim_ptr, int32_t* elim, int64_t* nops_h, void* stream);
+                  const int32_t* diag_pos, int milu, int64_t min_cand, const int32_t* cls,
+                  int8_t* heavy, int64_t* elim_ptr, int32_t* elim, int64_t* nops_h, void* stream);
 
 /* Class-aware schedule used by jv_factor / jv_solve: rows (nullable = 0..m-1)
  * stably sorted by key = 2*level + class; class-0 rows of a level go 32 to a

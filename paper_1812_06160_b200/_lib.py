@@ -31,6 +31,8 @@ _SIGS = {
     "jv_status": [_I32P],
     "jv_set_spin_limit": [ctypes.c_uint],
     "jv_set_backoff": [ctypes.c_uint],
+    "jv_set_gate": [ctypes.c_uint],
+    "jv_set_poll": [ctypes.c_uint],
     "jv_set_trace": [_P, ctypes.c_longlong],
     "jv_test_ddiv": [c_int32, _P, _P, _P, _P],
     "jv_spmv_tile": [],
@@ -53,7 +55,7 @@ _SIGS = {
     "jv_free_host": [c_void_p],
     "jv_factor": [c_int32, _P, _P, _P, _P, _P, c_double, c_int, _P, _P, c_int32, c_int32, _P,
                   c_uint32, _P, _P, _P, _P, _P, _P],
-    "jv_elim_lists": [c_int32, _P, _P, _P, c_int, c_int64, _P, _P, _P, POINTER(c_int64), _P],
+    "jv_elim_lists": [c_int32, _P, _P, _P, c_int, c_int64, _P, _P, _P, _P, POINTER(c_int64), _P],
     "jv_solve": [c_int, c_int32, _P, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, c_uint32, _P, _P],
     "jv_check_zero_diag": [c_int32, _P, _P, _P, _P],
     "jv_build_batches": [c_int32, _P, _P, _I32P, _P],

@@ -128,6 +128,19 @@ extern "C" int jv_set_backoff(unsigned cap_ns) {
   return JV_OK;
 }
 
+extern "C" int jv_set_gate(unsigned mask) {
+  cudaError_t e = cudaMemcpyToSymbol(jv::g_gate, &mask, sizeof(unsigned));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_gate");
+  return JV_OK;
+}
+
+extern "C" int jv_set_poll(unsigned cap_ns) {
+  if (cap_ns < 16) cap_ns = 16;
+  cudaError_t e = cudaMemcpyToSymbol(jv::g_poll_cap, &cap_ns, sizeof(unsigned));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_poll");
+  return JV_OK;
+}
+
 extern "C" int jv_set_spin_limit(unsigned limit) {
   cudaError_t e = cudaMemcpyToSymbol(jv::g_spin_limit, &limit, sizeof(unsigned));
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_spin_limit");

@@ -16,7 +16,7 @@ constexpr int kElimOut = 1 << 30;   // == factor.cu kOut
 // per-row candidate volume -> heavy flag, and the row's count of list pairs
 __global__ void elim_heavy_kernel(int n, const int32_t* rs, const int32_t* col,
                                   const int32_t* diag, int milu, long long min_cand,
-                                  int8_t* heavy, int32_t* npairs) {
+                                  const int32_t* cls, int8_t* heavy, int32_t* npairs) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int a = rs[r], len = rs[r + 1] - a, nL = diag[r] - a;
     long long cand = 0;
@@ -25,9 +25,15 @@ __global__ void elim_heavy_kernel(int n, const int32_t* rs, const int32_t* col,
       const long long ulen = rs[c + 1] - diag[c] - 1, rem = len - k - 1;
       cand += milu ? ulen : min(ulen, rem);
     }
-    const bool h = cand > min_cand;
-    heavy[r] = h ? 1 : 0;
-    npairs[r] = h ? nL : 0;
+    // 2: heavy (own path); 1: warp-path row with its list; 0: no list.
+    // Tentative: elim_refine_kernel promotes a listed row to 2 once the
+    // actual op counts show a 32-pivot chunk over the warp op list.
+    int f = 0;
+    if (nL > 0 && cand > min_cand) f = min_cand < 256 ? 2 : 1;
+    else if (nL > 0 && cls != nullptr) f = 1;
+    if (cls != nullptr && cls[r] == 0) f = 0;   // thread-path rows never read a list
+    heavy[r] = (int8_t)f;
+    npairs[r] = f ? nL : 0;
   }
 }
 
@@ -38,6 +44,17 @@ __global__ void elim_pairs_kernel(int n, const int32_t* rs, const int32_t* off, 
     for (int k = 0; k < m; ++k) {
       prow[b + k] = r;
       ppos[b + k] = rs[r] + k;
+    }
+  }
+}
+
+__global__ void elim_refine_kernel(int n, const int32_t* rs, const int32_t* diag,
+                                   const long long* eptr, int8_t* heavy) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (heavy[r] != 1) continue;
+    const int a = rs[r], nL = diag[r] - a;
+    for (int k0 = 0; k0 < nL; k0 += 32) {
+      if (eptr[a + min(k0 + 32, nL)] - eptr[a + k0] > 256) { heavy[r] = 2; break; }
     }
   }
 }
@@ -104,7 +121,8 @@ __global__ void __launch_bounds__(256) elim_match_kernel(
 }  // namespace
 
 extern "C" int jv_elim_lists(int32_t n, const int32_t* row_start, const int32_t* col,
-                             const int32_t* diag_pos, int milu, int64_t min_cand, int8_t* heavy,
+                             const int32_t* diag_pos, int milu, int64_t min_cand,
+                             const int32_t* cls, int8_t* heavy,
                              int64_t* elim_ptr, int32_t* elim, int64_t* nops_h, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   *nops_h = 0;
@@ -115,7 +133,7 @@ extern "C" int jv_elim_lists(int32_t n, const int32_t* row_start, const int32_t*
   CK_CUDA(npairs.alloc(sizeof(int32_t) * (n + 1)), "alloc");
   CK_CUDA(off.alloc(sizeof(int32_t) * (n + 1)), "alloc");
   elim_heavy_kernel<<<grid_for(n), kSetupThreads, 0, s>>>(n, row_start, col, diag_pos, milu,
-                                                          (long long)min_cand, heavy,
+                                                          (long long)min_cand, cls, heavy,
                                                           (int32_t*)npairs.p);
   set_int_kernel<<<1, 1, 0, s>>>((int32_t*)npairs.p + n, 0);
   size_t tb = 0;
@@ -146,6 +164,8 @@ extern "C" int jv_elim_lists(int32_t n, const int32_t* row_start, const int32_t*
   CK_CUDA(tmp2.alloc(tb2), "alloc");
   CK_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.p, tb2, (long long*)cnt.p, (long long*)elim_ptr,
                                         nnz + 1, s), "scan");
+  elim_refine_kernel<<<grid_for(n), kSetupThreads, 0, s>>>(n, row_start, diag_pos,
+                                                           (const long long*)elim_ptr, heavy);
   long long total = 0;
   CK_CUDA(cudaMemcpyAsync(&total, elim_ptr + nnz, sizeof(long long), cudaMemcpyDeviceToHost, s),
           "copy");

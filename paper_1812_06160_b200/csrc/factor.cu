@@ -38,6 +38,16 @@
 
 namespace {
 
+// JV_HEAVY_PROFILE (diagnostic builds only): per-phase clock64 sums of the
+// warp / heavy row paths, written to the batch trace (tools/trace.py)
+#ifdef JV_HEAVY_PROFILE
+#define HP_T0(v) long long v = clock64()
+#define HP_ADD(acc, v) acc += clock64() - v
+#else
+#define HP_T0(v)
+#define HP_ADD(acc, v)
+#endif
+
 constexpr int kR = 8;       // thread path: row entries
 constexpr int kP = 4;       // thread path: pivots (strict-lower entries)
 constexpr int kU = 4;       // thread path: strict-upper entries per pivot row
@@ -288,7 +298,7 @@ JV_INLINE unsigned short_gather(const FactorArgs& A, const ShortRow& R, Slice S,
     }
     if (__any_sync(mask, miss)) {
       if (ns) __nanosleep(ns);
-      ns = ns ? min(2 * ns, 128u) : 16u;
+      ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
       if (++spins == jv::g_spin_limit) {
         atomicExch(&jv::g_hang, 1);
         break;
@@ -486,7 +496,7 @@ JV_INLINE void sfp_finish(const FactorArgs& A, int r, SfpRow& F, unsigned mask, 
     }
     if (__any_sync(mask, miss)) {
       if (ns) __nanosleep(ns);
-      ns = ns ? min(2 * ns, 128u) : 16u;
+      ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
       if (++spins == jv::g_spin_limit) {
         atomicExch(&jv::g_hang, 1);
         break;
@@ -519,7 +529,7 @@ JV_INLINE double warp_value(const FactorArgs& A, bool need, int c, int q) {
     }
     if (__any_sync(0xffffffffu, miss)) {
       if (ns) __nanosleep(ns);
-      ns = ns ? min(2 * ns, 128u) : 16u;
+      ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
       if (++spins == jv::g_spin_limit) {
         atomicExch(&jv::g_hang, 1);
         break;
@@ -530,13 +540,17 @@ JV_INLINE double warp_value(const FactorArgs& A, bool need, int c, int q) {
 }
 
 // Apply all pivots of row r with the whole warp.
-JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
+JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W, const jv::Trace& T,
+                        int bt) {
+  [[maybe_unused]] long long wp_load = 0, wp_struct = 0, wp_gate = 0, wp_gather = 0, wp_elim = 0;
+  HP_T0(wp_start);
   const unsigned full = 0xffffffffu;
   const int rs = A.row_start[r], re = A.row_start[r + 1];
   const int len = re - rs;
   const int dloc = A.diag[r] - rs;
   const int nL = dloc;
   const bool cached = len <= kWarpRow;
+  const bool listed = A.heavy != nullptr && A.heavy[r] == 1;
   double* av = cached ? W.val : A.val + rs;
   const int* ac = cached ? W.col : A.col + rs;
   if (cached) {
@@ -547,20 +561,37 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
     __syncwarp();
   }
   const double thresh = A.tau > 0.0 ? jv::dmul(A.tau, A.norms[r]) : 0.0;
+  HP_ADD(wp_load, wp_start);
 
   for (int k0 = 0; k0 < nL;) {
+    HP_T0(t_struct);
     const int kc = min(32, nL - k0);
     int c = -1, d = 0, ce = 0;
+    long long e1 = 0;
     if (lane < kc) {
       c = ac[k0 + lane];
       d = A.diag[c];
-      ce = A.row_start[c + 1];
+      if (listed) e1 = A.elim_ptr[rs + k0 + lane + 1];
+      else ce = A.row_start[c + 1];
       W.pivc[lane] = c;
     }
     // ---- structure of the chunk: op list (q, target) per pivot
     int nops = 0, kdone = 0;
     bool direct = false;
-    for (int kk = 0; kk < kc; ++kk) {
+    if (listed) {
+      // precomputed (jv_elim_lists): the chunk's ops are one contiguous run
+      // (a listed row has <= kWarpOps candidates in total)
+      const long long E0 = A.elim_ptr[rs + k0];
+      if (lane < kc) W.opend[lane] = (int)(e1 - E0);
+      nops = (int)(__shfl_sync(full, e1, kc - 1) - E0);
+      for (int o = lane; o < nops; o += 32) {
+        const int2 op = __ldg(A.elim + E0 + o);
+        W.opq[o] = op.x;
+        W.opw[o] = op.y;
+      }
+      kdone = kc;
+    }
+    for (int kk = 0; kk < kc && !listed; ++kk) {
       const int k = k0 + kk;
       const int dk = __shfl_sync(full, d, kk), cek = __shfl_sync(full, ce, kk);
       const int ulen = cek - dk - 1, rem = len - k - 1;
@@ -679,32 +710,81 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
     }
 
     // ---- gate on the newest pivot of the chunk, then one converged gather
+    HP_ADD(wp_struct, t_struct);
+    HP_T0(t_gate);
     int g = (lane < kdone && c >= A.ready_below) ? c : -1, gq = d;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const int og = __shfl_xor_sync(full, g, o), oq = __shfl_xor_sync(full, gq, o);
       if (og > g) { g = og; gq = oq; }
     }
-    if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, gq, A.epoch);
+    if (lane == 0 && g >= 0 && (jv::g_gate & 1)) jv::mbox_gate(A.mbox, gq, A.epoch);
     __syncwarp();
-    const double dv = warp_value(A, lane < kdone, c, d);
-    for (int base = 0; base < nops; base += 32) {
-      const int o = base + lane;
-      int ck = 0, q = 0;
-      if (o < nops) {
-        // pivot of op o: first kk with opend[kk] > o
-        int lo = 0, hi = kdone - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (W.opend[mid] > o) hi = mid; else lo = mid + 1;
+    HP_ADD(wp_gate, t_gate);
+    HP_T0(t_gather);
+    // every probe of the chunk (pivot diagonals + up to kWarpOps op values)
+    // is issued before any is checked: one memory round trip, then
+    // converged waits only for the packets that were not there yet
+    constexpr int kSlots = kWarpOps / 32;
+    double dv = 0.0;
+    bool dmiss = false;
+    {
+      const bool have = lane < kdone;
+      Probe pd{0, 0};
+      if (have && c < A.ready_below) dv = __ldcg(A.val + d);
+      else if (have) pd = probe_issue(A.mbox, d);
+      Probe po[kSlots];
+      int pk[kSlots];
+#pragma unroll
+      for (int i = 0; i < kSlots; ++i) {
+        const int o = i * 32 + lane;
+        pk[i] = 0;
+        po[i] = Probe{0, 0};
+        if (o < nops) {
+          int ck = 0;
+          if (A.ready_below > 0) {
+            // pivot of op o: first kk with opend[kk] > o
+            int lo = 0, hi = kdone - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (W.opend[mid] > o) hi = mid; else lo = mid + 1;
+            }
+            ck = W.pivc[lo];
+          }
+          pk[i] = ck;
+          if (ck < A.ready_below) W.opv[o] = __ldcg(A.val + W.opq[o]);
+          else po[i] = probe_issue(A.mbox, W.opq[o]);
         }
-        ck = W.pivc[lo];
-        q = W.opq[o];
       }
-      const double v = warp_value(A, o < nops, ck, q);
-      if (o < nops) W.opv[o] = v;
+      if (have && c >= A.ready_below) {
+        if (probe_ok(pd, A.epoch)) dv = probe_val(pd);
+        else dmiss = true;
+      }
+      unsigned omiss = 0;
+#pragma unroll
+      for (int i = 0; i < kSlots; ++i) {
+        const int o = i * 32 + lane;
+        if (o < nops && pk[i] >= A.ready_below) {
+          if (probe_ok(po[i], A.epoch)) W.opv[o] = probe_val(po[i]);
+          else omiss |= 1u << i;
+        }
+      }
+      if (__any_sync(full, dmiss)) {
+        const double v = warp_value(A, dmiss, c, d);
+        if (dmiss) dv = v;
+      }
+      if (__any_sync(full, omiss != 0)) {
+        for (int i = 0; i < kSlots; ++i) {
+          const bool m = (omiss >> i) & 1;
+          const int o = i * 32 + lane;
+          const double v = warp_value(A, m, pk[i], m ? W.opq[o] : 0);
+          if (m) W.opv[o] = v;
+        }
+      }
     }
     __syncwarp();
+    HP_ADD(wp_gather, t_gather);
+    HP_T0(t_elim);
 
     // ---- elimination, pivot by pivot
     for (int kk = 0, o0 = 0; kk < kdone; ++kk) {
@@ -714,7 +794,10 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
       double l = 0.0;
       int drop = 0;
       if (lane == 0) {
-        l = jv::ddiv(av[k], dk);
+        bool slow;
+        const double a = av[k];
+        l = jv::ddiv_fast(a, dk, slow);
+        if (slow) l = __ddiv_rn(a, dk);
         drop = A.tau > 0.0 && fabs(l) < thresh;
         av[k] = drop ? 0.0 : l;
       }
@@ -736,6 +819,7 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
       o0 = o1;
       __syncwarp();
     }
+    HP_ADD(wp_elim, t_elim);
     k0 += kdone;
   }
 
@@ -747,6 +831,16 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W) {
   }
   if (lane == 0 && av[dloc] == 0.0) atomicMin(A.err, r);
   __syncwarp();
+#ifdef JV_HEAVY_PROFILE
+  if (lane == 0) {
+    jv::trace_word(T, bt, 7, ((unsigned long long)wp_load << 32) | (unsigned)wp_struct);
+    jv::trace_word(T, bt, 13, wp_gate);
+    jv::trace_word(T, bt, 14, ((unsigned long long)wp_gather << 32) | (unsigned)wp_elim);
+    jv::trace_word(T, bt, 15, clock64() - wp_start);
+  }
+#else
+  (void)T; (void)bt;
+#endif
 }
 
 // Heavy rows (power-law hubs: thousands of pivots whose U rows hold
@@ -828,14 +922,6 @@ struct HeavyStream {
     issue_pkts(i + 3);
   }
 };
-
-#ifdef JV_HEAVY_PROFILE
-#define HP_T0(v) long long v = clock64()
-#define HP_ADD(acc, v) acc += clock64() - v
-#else
-#define HP_T0(v)
-#define HP_ADD(acc, v)
-#endif
 
 // u value of ring entry e (pivot row c); false when its packet is stale
 JV_INLINE bool ring_value(const FactorArgs& A, const Ring& R, int e, int c, double& u) {
@@ -1098,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
       const int og = __shfl_xor_sync(full, g, o), oq = __shfl_xor_sync(full, gq, o);
       if (og > g) { g = og; gq = oq; }
     }
-    if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, gq, A.epoch);
+    if (lane == 0 && g >= 0 && (jv::g_gate & 1)) jv::mbox_gate(A.mbox, gq, A.epoch);
     __syncwarp();
     if (lane == 0) jv::trace_mark(T, b, 3);
     const unsigned smask = __ballot_sync(full, sfp);
@@ -1110,8 +1196,8 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
       const int rr = __shfl_sync(full, r, src);
-      if (A.heavy != nullptr && A.heavy[rr]) heavy_row(A, rr, lane, &heavy_busy, hbuf, T, b);
-      else warp_row(A, rr, lane, W);
+      if (A.heavy != nullptr && A.heavy[rr] == 2) heavy_row(A, rr, lane, &heavy_busy, hbuf, T, b);
+      else warp_row(A, rr, lane, W, T, b);
     }
     __syncwarp();
     if (lane == 0) jv::trace_mark(T, b, 4);

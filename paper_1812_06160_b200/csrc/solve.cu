@@ -64,7 +64,7 @@ JV_INLINE void gather_conv(const SolveArgs& A, const int (&c)[N], double (&v)[N]
     }
     if (__any_sync(mask, miss)) {
       if (ns) __nanosleep(ns);
-      ns = ns ? min(2 * ns, 128u) : 16u;
+      ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
       if (++spins == jv::g_spin_limit) {
         atomicExch(&jv::g_hang, 1);
         break;
@@ -138,12 +138,12 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
       g = (active && p1 > p0) ? __ldg(A.col + p0) : 0x7fffffff;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) g = min(g, __shfl_xor_sync(full, g, o));
-      if (lane == 0 && g != 0x7fffffff) jv::mbox_gate(A.mbox, g, A.epoch);
+      if (lane == 0 && g != 0x7fffffff && (jv::g_gate & 2)) jv::mbox_gate(A.mbox, g, A.epoch);
     } else {
       g = (active && p1 > p0) ? __ldg(A.col + p1 - 1) : -1;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) g = max(g, __shfl_xor_sync(full, g, o));
-      if (lane == 0 && g >= 0) jv::mbox_gate(A.mbox, g, A.epoch);
+      if (lane == 0 && g >= 0 && (jv::g_gate & 2)) jv::mbox_gate(A.mbox, g, A.epoch);
     }
     __syncwarp();
     const bool small = p1 - p0 <= kThreadDeps;

@@ -365,6 +365,7 @@ class DevIlu:
 
     # heavy rows: structural matches precomputed once per pattern (jv_elim_lists)
     ELIM_MIN_CAND = 256
+    ELIM_WARP_ROWS = True     # lists for every warp-path row, not only heavy ones
 
     def elim_lists(self):
         """(heavy, elim_ptr, elim) device buffers, or None if no row is heavy."""
@@ -375,7 +376,8 @@ class DevIlu:
             eptr = t.empty(self.nnz + 1, dtype=t.int64, device="cuda")
             nops = ctypes.c_int64(0)
             args = [self.n, ptr(self.row_start), ptr(self.col), ptr(self.diag_pos), int(self.milu),
-                    self.ELIM_MIN_CAND, ptr(heavy), ptr(eptr)]
+                    self.ELIM_MIN_CAND, ptr(self._classes("factor")) if self.ELIM_WARP_ROWS else None,
+                    ptr(heavy), ptr(eptr)]
             _lib.call("jv_elim_lists", *args, None, ctypes.byref(nops), stream())
             lists = None
             if nops.value > 0:

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--spin", type=int, default=24)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rmat-seed", type=int, default=-1)
+    ap.add_argument("--gate", type=int, default=None)
+    ap.add_argument("--poll", type=int, default=None)
     args = ap.parse_args()
     import torch
     import paper_1812_06160_b200 as jv
@@ -33,6 +35,10 @@ def main():
     _lib.call("jv_set_spin_limit", 1 << args.spin)
     if args.backoff is not None:
         _lib.call("jv_set_backoff", args.backoff)
+    if args.gate is not None:
+        _lib.call("jv_set_gate", args.gate)
+    if args.poll is not None:
+        _lib.call("jv_set_poll", args.poll)
     t0 = time.time()
     if args.rmat_seed >= 0:
         a, base, s = W.rmat(18, args.rmat_seed), None, W.CONFIGS["c5"]
