@@ -79,7 +79,8 @@ int jv_test_ddiv(int32_t n, const double* a, const double* b, double* out, void*
  * Row sums are accumulated in ascending column order without FMA, so the
  * result is bitwise equal to the reference for every row of up to
  * jv_spmv_tile() entries; longer rows use a tree sum (within 1e-12).
- * tile_rows (nullable) is the jv_spmv_plan output, int32[ntiles+1] with
+ * tile_rows (nullable) is the jv_spmv_plan output, int32[2*(ntiles+1)]
+ * (first row of each tile boundary and that row's first nonzero) with
  * ntiles = max(1, ceil(nnz / jv_spmv_tile())).                           */
 int jv_spmv_tile(void);
 int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, int32_t* tile_rows,

@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_uint32, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjv.so")
+LIB_PATH = os.environ.get("JV_LIB") or os.path.join(_HERE, "libjv.so")  # JV_LIB: diagnostic builds
 
 
 class BackendUnavailable(RuntimeError):

@@ -53,7 +53,10 @@ constexpr int kP = 4;       // thread path: pivots (strict-lower entries)
 constexpr int kU = 4;       // thread path: strict-upper entries per pivot row
 constexpr int kWarpRow = 128;   // warp path: row entries cached in smem
 constexpr int kWarpOps = 256;   // warp path: op list capacity per chunk
-constexpr int kFactorWarps = 8; // warps per CTA
+#ifndef JV_FACTOR_WARPS
+#define JV_FACTOR_WARPS 8
+#endif
+constexpr int kFactorWarps = JV_FACTOR_WARPS; // warps per CTA (one CTA per SM)
 constexpr int kOut = 1 << 30;   // op target flag: out-of-pattern (MILU -> diagonal)
 
 struct FactorArgs {
@@ -131,7 +134,11 @@ JV_INLINE double pivot_value(const FactorArgs& A, int c, int q) {
 constexpr int kSlotsI = kR + 2 * kP + kP * kU;    // cj | dq | ulen | op list
 constexpr int kSlotsD = kR + kP + kP * kU + kP;   // a | dv | uv | lspec
 constexpr int kThreads = kFactorWarps * 32;
-constexpr size_t kArenaBytes = sizeof(WarpArena) * kFactorWarps;
+// The warp arena of a warp-path row lives in the warp's own slice block
+// (a warp runs one batch at a time: thread-path slices, warp-path arena and
+// heavy-row ring never coexist), so the slab is slices + the heavy buffer.
+constexpr size_t kArenaBytes = 0;
+static_assert(sizeof(WarpArena) <= 32 * kSlotsD * sizeof(double), "arena must fit a slice block");
 
 extern __shared__ __align__(16) unsigned char jv_factor_smem[];
 
@@ -858,7 +865,10 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W, cons
 //    HBM), so the per-step read-modify-writes are shared-memory latency.
 constexpr int kRing = 512;          // ops per warp ring
 constexpr int kWin = 64;            // ops per window (2 per lane)
-constexpr int kHeavyCap = 10752;    // row entries in the CTA heavy buffer
+// row entries in the CTA heavy buffer: what the slices leave of the SM's
+// shared memory (two halves)
+constexpr int kHeavyCap =
+    (int)(((232448 - 1024 - (size_t)kThreads * (kSlotsI * 4 + kSlotsD * 8)) / sizeof(double)) & ~63);
 constexpr size_t kSliceBytes = (size_t)kThreads * (kSlotsI * 4 + kSlotsD * 8);
 static_assert(kSlotsI * 32 >= 2 * kRing && kSlotsD * 32 >= 2 * kRing, "ring must fit the slices");
 
@@ -1148,10 +1158,10 @@ constexpr size_t kFactorSmem = kArenaBytes + kSliceBytes + sizeof(double) * kHea
 static_assert(kFactorSmem <= 232448 - 64, "factor kernel shared memory");
 
 __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
-  WarpArena* arena = reinterpret_cast<WarpArena*>(jv_factor_smem);
+
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  WarpArena& W = arena[threadIdx.x >> 5];
+  WarpArena& W = *reinterpret_cast<WarpArena*>(slice_doubles(threadIdx.x >> 5));
   const Slice S{(int)threadIdx.x};
   const jv::Trace T = jv::trace_begin();
   const int nw = (gridDim.x * blockDim.x) >> 5;

@@ -18,8 +18,14 @@
 
 namespace {
 
-constexpr int kSpmvThreads = 256;
-constexpr int kTile = 2048;          // nonzeros per CTA tile
+#ifndef JV_SPMV_THREADS
+#define JV_SPMV_THREADS 128
+#endif
+#ifndef JV_SPMV_TILE
+#define JV_SPMV_TILE 640
+#endif
+constexpr int kSpmvThreads = JV_SPMV_THREADS;
+constexpr int kTile = JV_SPMV_TILE;  // nonzeros per CTA tile
 constexpr int kBuf = 2 * kTile;      // shared products: any row <= kTile fits
 
 // first row in [0, n) whose start is >= key (n if none)
@@ -38,7 +44,8 @@ __global__ void spmv_plan_kernel(int n, int nnz, int ntiles, const int32_t* rs, 
     if (t == 0) r = 0;
     else if (t == ntiles) r = n;
     else r = row_lower_bound(rs, n, t * kTile);
-    tile_rows[t] = r;
+    tile_rows[2 * t] = r;
+    tile_rows[2 * t + 1] = rs[r];
   }
 }
 
@@ -50,24 +57,43 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
   __shared__ double red[kSpmvThreads / 32];
   const int t = blockIdx.x;
   const int ntiles = gridDim.x;
-  int r0, r1;
+  int r0, r1, p0, p1;
   if (tile_rows) {
-    r0 = __ldg(tile_rows + t);
-    r1 = __ldg(tile_rows + t + 1);
+    // (first row, its first nonzero) of this tile and the next: one load
+    const int2 a = __ldg(reinterpret_cast<const int2*>(tile_rows) + t);
+    const int2 b = __ldg(reinterpret_cast<const int2*>(tile_rows) + t + 1);
+    r0 = a.x; p0 = a.y; r1 = b.x; p1 = b.y;
   } else {
     r0 = (t == 0) ? 0 : row_lower_bound(rs, n, t * kTile);
     r1 = (t == ntiles - 1) ? n : row_lower_bound(rs, n, (t + 1) * kTile);
+    p0 = __ldg(rs + r0);
+    p1 = __ldg(rs + r1);
   }
   if (r0 >= r1) return;
-  const int p0 = __ldg(rs + r0);
   int rlast = r1;
-  int p1 = __ldg(rs + r1);
   if (p1 - p0 > kBuf) {        // the tile's last row is longer than kTile
     rlast = r1 - 1;
     p1 = __ldg(rs + rlast);
   }
-  for (int p = p0 + threadIdx.x; p < p1; p += kSpmvThreads)
-    prod[p - p0] = jv::dmul(__ldcs(val + p), __ldg(x + __ldcs(col + p)));
+  // products, kU independent load chains per thread in flight (col -> x)
+  constexpr int kU = 8;
+  for (int b = p0 + threadIdx.x; b < p1; b += kSpmvThreads * kU) {
+    int c[kU];
+    double v[kU], xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = b + u * kSpmvThreads;
+      c[u] = p < p1 ? __ldcs(col + p) : 0;
+      v[u] = p < p1 ? __ldcs(val + p) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = b + u * kSpmvThreads;
+      if (p < p1) prod[p - p0] = jv::dmul(v[u], xv[u]);
+    }
+  }
   __syncthreads();
   for (int r = r0 + threadIdx.x; r < rlast; r += kSpmvThreads) {
     const int a = __ldg(rs + r) - p0, b = __ldg(rs + r + 1) - p0;

@@ -218,7 +218,7 @@ class DevCsr:
         if self._tile_rows is None:
             tile = _lib.load().jv_spmv_tile()
             ntiles = max(1, -(-self.nnz // tile))
-            self._tile_rows = empty_i32(ntiles + 1)
+            self._tile_rows = empty_i32(2 * (ntiles + 1))
             _lib.call("jv_spmv_plan", self.n, self.nnz, ptr(self.row_start), ptr(self._tile_rows),
                       stream())
         return self._tile_rows
