@@ -411,7 +411,10 @@ def run_mine(args):
 
     multi = None
     if world > 1 and not batched:
-        multi = {"spmv_dist": measure_spmv_dist(plan, max(K, 20), world, rank)}
+        try:
+            multi = {"spmv_dist": measure_spmv_dist(plan, max(K, 20), world, rank)}
+        except Exception as e:   # never lose the main line to the extra measurement
+            multi = {"spmv_dist": {"error": repr(e)[:200]}}
 
     peak, peak_kind = peaks()
     # per-GPU algorithmic bytes (every rank factors its own matrix / shard)
