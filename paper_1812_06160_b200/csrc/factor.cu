@@ -510,7 +510,12 @@ JV_INLINE void sfp_finish(const FactorArgs& A, int r, SfpRow& F, unsigned mask, 
       }
     }
   }
-  if ((threadIdx.x & 31) == __ffs(mask) - 1) jv::trace_mark(T, cur_batch, 7);
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) {
+    jv::trace_mark(T, cur_batch, 7);
+#ifdef JV_HEAVY_PROFILE
+    jv::trace_word(T, cur_batch, 13, spins);
+#endif
+  }
   sfp_compute(A, r, F);
 }
 

@@ -24,7 +24,8 @@
 namespace {
 
 constexpr int kThreadDeps = 32;   // longer rows take the warp path
-constexpr int kProbe = 8;         // dependency values probed together per round
+constexpr int kProbe = 12;        // dependency values probed together per round (swept 8-16)
+constexpr int kWarpBlock = 128;   // warp path: dependencies per prefetched block
 
 struct SolveArgs {
   const int32_t* row_start;
@@ -93,21 +94,60 @@ JV_INLINE double fold_deps(const SolveArgs& A, int p0, int p1, double s, unsigne
   return s;
 }
 
-// warp path: same chain, 32 dependencies per round (lane t gathers one,
-// products formed in parallel, one lane keeps the subtraction order)
-JV_INLINE double fold_deps_warp(const SolveArgs& A, int p0, int p1, double s, int lane) {
+// warp path: same chain in blocks of 128 dependencies: the probes of block
+// k+1 are issued before block k is folded (one L2 round trip hides behind
+// the fold), products go to shared memory and one lane keeps the
+// subtraction order (8-cycle DSUB chain, loads pipelined).  s is valid in
+// lane 0.
+JV_INLINE double fold_deps_warp(const SolveArgs& A, int p0, int p1, double s, int lane,
+                                double* sp) {
   const unsigned full = 0xffffffffu;
-  for (int g = p0; g < p1; g += 32) {
-    const int p = g + lane;
-    int c[1] = {p < p1 ? __ldg(A.col + p) : 0};
-    double v[1] = {0.0};
-    gather_conv<1>(A, c, v, p < p1 ? 1u : 0u, full);
-    const double prod = p < p1 ? jv::dmul(__ldg(A.val + p), v[0]) : 0.0;
-    const int m = min(32, p1 - g);
-    for (int t = 0; t < m; ++t) {
-      const double pt = __shfl_sync(full, prod, t);
-      s = jv::dsub(s, pt);
+  constexpr int K = kWarpBlock / 32;
+  int c[K];
+  double v[K], x[K];
+  unsigned long long w0[K], w1[K];
+  auto issue = [&](int g) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int p = g + 32 * j + lane;
+      c[j] = p < p1 ? __ldg(A.col + p) : 0;
+      v[j] = p < p1 ? __ldg(A.val + p) : 0.0;
+      if (p < p1)
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(w0[j]), "=l"(w1[j]) : "l"(A.mbox + 2 * (long long)c[j]));
     }
+  };
+  auto settle = [&](int g) {
+    unsigned miss = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int p = g + 32 * j + lane;
+      x[j] = 0.0;
+      if (p < p1) {
+        if ((uint32_t)(w0[j] >> 32) == A.epoch && (uint32_t)(w1[j] >> 32) == A.epoch)
+          x[j] = __longlong_as_double((long long)((w0[j] & 0xffffffffull) | (w1[j] << 32)));
+        else
+          miss |= 1u << j;
+      }
+    }
+    if (__any_sync(full, miss != 0)) gather_conv<K>(A, c, x, miss, full);
+  };
+  if (p0 >= p1) return s;
+  issue(p0);
+  for (int g = p0, blk = 0; g < p1; g += kWarpBlock, blk ^= 1) {
+    settle(g);
+    double* buf = sp + blk * kWarpBlock;
+#pragma unroll
+    for (int j = 0; j < K; ++j) buf[32 * j + lane] = jv::dmul(v[j], x[j]);
+    __syncwarp();
+    const int gn = g + kWarpBlock;
+    if (gn < p1) issue(gn);     // next block's probes fly during the fold
+    if (lane == 0) {
+      const int m = min(kWarpBlock, p1 - g);
+#pragma unroll 8
+      for (int t = 0; t < m; ++t) s = jv::dsub(s, buf[t]);
+    }
+    __syncwarp();
   }
   return s;
 }
@@ -116,6 +156,8 @@ template <bool kBackward>
 __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  __shared__ double warp_prod[8][2 * kWarpBlock];
+  double* sp = warp_prod[threadIdx.x >> 5];
   const int W = (gridDim.x * blockDim.x) >> 5;
   const jv::Trace T = jv::trace_begin();
   for (;;) {
@@ -150,7 +192,12 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
     const unsigned smask = __ballot_sync(full, active && small);
     if (active && small) {
       double s = fold_deps(A, p0, p1, A.in[r], smask);
-      if (kBackward) s = jv::ddiv(s, __ldg(A.val + dp));
+      if (kBackward) {
+        const double d = __ldg(A.val + dp);
+        bool slow;
+        const double q = jv::ddiv_fast(s, d, slow);
+        s = slow ? __ddiv_rn(s, d) : q;
+      }
       A.out[r] = s;
       jv::mbox_put(A.mbox, r, s, A.epoch);
     }
@@ -160,7 +207,7 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
       pend &= pend - 1;
       const int rr = __shfl_sync(full, r, src);
       const int q0 = __shfl_sync(full, p0, src), q1 = __shfl_sync(full, p1, src);
-      double s = fold_deps_warp(A, q0, q1, A.in[rr], lane);
+      double s = fold_deps_warp(A, q0, q1, A.in[rr], lane, sp);
       if (lane == 0) {
         if (kBackward) s = jv::ddiv(s, __ldg(A.val + __ldg(A.diag + rr)));
         A.out[rr] = s;

@@ -1,7 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-B="python bench.py --steps 3 --warmup 3 --no-cpu"
-$B > gpurun_out/plain_bench.json 2> gpurun_out/plain_bench.err && \
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv $B > gpurun_out/ncu_launch.log 2>&1
-echo "launch list rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"factor_kernel|solve_kernel|spmv_stream" -s 12 -c 4 -o gpurun_out/prof_r01_c2 $B > gpurun_out/ncu_full.log 2>&1
-echo "full rc=$?"
+timeout 900 python -m pytest tests/ -q -x -m gpu 2>&1 | tail -1 | sed 's/warn/w/'
+for c in c1 c2 c3 c4; do timeout 300 python tools/diag.py --config $c > gpurun_out/d.log 2>&1; python -c "import json; d=[json.loads(l) for l in open('gpurun_out/d.log') if l.startswith('{')][-1]; print(d['config'], 'f', round(min(d['factor_ms']),3), 'fw', round(min(d['fwd_ms']),3), 'bw', round(min(d['bwd_ms']),3))"; done
+timeout 300 python tools/trace.py --config c4 > /dev/null 2>&1; ls gpurun_out/trace_c4.npz
