@@ -179,7 +179,10 @@ int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col, double* v
               const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
               int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
               int32_t* ticket, const int8_t* heavy, const int64_t* elim_ptr,
-              const int32_t* elim, void* stream);
+              const int32_t* elim, const int8_t* batch_class, void* stream);
+/* batch_class (nullable): class of each batch of the schedule (0: up to 32
+ * thread-path rows, 1: a pair of listed warp rows, 2: one warp row), i.e.
+ * key % 3 of its first row under jv_build_schedule_n(nclass 3).          */
 /* `ready_below`: rows with index < ready_below were factored by an earlier
  * call (the upper stage before the lower-tail call, lower.py:273-318) and are
  * read from val directly instead of the mailbox. */
@@ -214,7 +217,9 @@ int jv_build_batches(int32_t nlev, const int32_t* level_ptr, int32_t* batch_ptr,
  * warp-path rows.  A listed row is heavy (flag 2, the power-law path) when
  * one of its 32-pivot chunks holds more than 256 ops (the warp op list) —
  * or always when min_cand < 256 (diagnostic setting); otherwise flag 1 (the
- * warp path reads its op list instead of searching).  Thread-path
+ * warp path reads its op list instead of searching): 1 when the row is
+ * also pairable (length <= 64, no pivot with more than 160 ops: two such
+ * rows of one level share a warp, a half each), else 3.  Thread-path
  * rows (cls 0) get none (flag 0).  heavy[n] (int8) holds the flags;
  * elim_ptr[nnz+1] gives each strict-lower entry p of a listed row its ops
  * [elim_ptr[p], elim_ptr[p+1]) (0-length for every other entry);
@@ -233,6 +238,13 @@ int jv_elim_lists(int32_t n, const int32_t* row_start, const int32_t* col,
  * order[m], batch_ptr sized >= m + nkeys + 1; *nbatch_h (synchronises). */
 int jv_build_schedule(int32_t m, const int32_t* rows, const int32_t* keys, int32_t nkeys,
                       int32_t* order, int32_t* batch_ptr, int32_t* nbatch_h, void* stream);
+/* General form: key = nclass * level + class (nclass <= 4), class c rows
+ * `steps[c]` (host array) to a batch.  jv_build_schedule = nclass 2, steps
+ * {32, 1}; the factor uses nclass 3, steps {32, 2, 1} (thread rows, pairs
+ * of listed warp rows, single warp rows).                                */
+int jv_build_schedule_n(int32_t m, const int32_t* rows, const int32_t* keys, int32_t nkeys,
+                        int32_t nclass, const int32_t* steps, int32_t* order, int32_t* batch_ptr,
+                        int32_t* nbatch_h, void* stream);
 /* row classes: factor (thread path iff <= 8 entries, <= 4 pivots, pivots'
  * U rows <= 4 entries, no MILU) and solve (thread path iff <= 32 deps) */
 int jv_classify_factor(int32_t n, const int32_t* row_start, const int32_t* col,

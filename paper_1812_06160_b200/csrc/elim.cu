@@ -30,7 +30,7 @@ __global__ void elim_heavy_kernel(int n, const int32_t* rs, const int32_t* col,
     // actual op counts show a 32-pivot chunk over the warp op list.
     int f = 0;
     if (nL > 0 && cand > min_cand) f = min_cand < 256 ? 2 : 1;
-    else if (nL > 0 && cls != nullptr) f = 1;
+    else if (cls != nullptr) f = 1;             // warp-path row (possibly no pivots)
     if (cls != nullptr && cls[r] == 0) f = 0;   // thread-path rows never read a list
     heavy[r] = (int8_t)f;
     npairs[r] = f ? nL : 0;
@@ -48,14 +48,22 @@ __global__ void elim_pairs_kernel(int n, const int32_t* rs, const int32_t* off, 
   }
 }
 
+// final flags of listed rows: 2 (heavy) when a 32-pivot chunk holds more
+// than 256 ops (factor.cu kWarpOps); else 1 (pairable: length <= 64 and no
+// pivot with more than 160 ops — factor.cu kPairRow / kPairOps) or 3
 __global__ void elim_refine_kernel(int n, const int32_t* rs, const int32_t* diag,
                                    const long long* eptr, int8_t* heavy) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     if (heavy[r] != 1) continue;
-    const int a = rs[r], nL = diag[r] - a;
+    const int a = rs[r], nL = diag[r] - a, len = rs[r + 1] - a;
+    int f = len <= 64 ? 1 : 3;
     for (int k0 = 0; k0 < nL; k0 += 32) {
-      if (eptr[a + min(k0 + 32, nL)] - eptr[a + k0] > 256) { heavy[r] = 2; break; }
+      if (eptr[a + min(k0 + 32, nL)] - eptr[a + k0] > 256) { f = 2; break; }
     }
+    if (f == 1)
+      for (int k = 0; k < nL; ++k)
+        if (eptr[a + k + 1] - eptr[a + k] > 160) { f = 3; break; }
+    heavy[r] = (int8_t)f;
   }
 }
 

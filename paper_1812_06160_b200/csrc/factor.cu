@@ -78,6 +78,7 @@ struct FactorArgs {
   const int8_t* heavy;        // nullable: rows with an elimination list
   const int64_t* elim_ptr;    // [nnz+1]: ops of L entry p = [elim_ptr[p], elim_ptr[p+1])
   const int2* elim;           // op = (q: U entry of the pivot row, w: target position | kOut)
+  const int8_t* bclass;       // nullable: batch class (0 thread rows, 1 row pair, 2 single row)
 };
 
 struct WarpArena {
@@ -551,6 +552,185 @@ JV_INLINE double warp_value(const FactorArgs& A, bool need, int c, int q) {
   return v;
 }
 
+// ------------------------------------------------------------ pair path
+//
+// Two listed warp-path rows of the same level (so independent) in one warp,
+// a half-warp each: the memory latency of one row's phases overlaps the
+// other's, doubling warp-row throughput (configs 3/4 are bound by warp
+// time per row).  Rows qualify at setup (jv_elim_lists flag 1): cached
+// length <= kPairRow, every pivot's ops <= kPairOps.
+constexpr int kPairRow = 64;
+constexpr int kPairOps = 160;
+
+struct HalfArena {
+  double val[kPairRow];
+  double opv[kPairOps];
+  int col[kPairRow];
+  int opq[kPairOps];
+  int opw[kPairOps];
+  int opend[16];
+  int pivc[16];
+};
+
+// converged wait inside one half-warp (mask = that half's lanes)
+JV_INLINE double half_value(const FactorArgs& A, bool need, int q, unsigned mask) {
+  double v = 0.0;
+  bool miss = need;
+  unsigned ns = 0, spins = 0;
+  while (__any_sync(mask, miss)) {
+    if (miss) {
+      const Probe p = probe_issue(A.mbox, q);
+      if (probe_ok(p, A.epoch)) {
+        v = probe_val(p);
+        miss = false;
+      }
+    }
+    if (__any_sync(mask, miss)) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
+      if (++spins == jv::g_spin_limit) {
+        atomicExch(&jv::g_hang, 1);
+        break;
+      }
+    }
+  }
+  return v;
+}
+
+JV_INLINE void pair_row(const FactorArgs& A, int r, int hl, unsigned hmask, HalfArena& H) {
+  const int rs = A.row_start[r], re = A.row_start[r + 1];
+  const int len = re - rs;
+  const int nL = A.diag[r] - rs;
+  double* av = H.val;
+  for (int i = hl; i < len; i += 16) {
+    H.col[i] = A.col[rs + i];
+    H.val[i] = __ldcs(A.val + rs + i);
+  }
+  __syncwarp(hmask);
+  const double thresh = A.tau > 0.0 ? jv::dmul(A.tau, A.norms[r]) : 0.0;
+  constexpr int kSlots = kPairOps / 16;
+
+  for (int k0 = 0; k0 < nL;) {
+    const int kc0 = min(16, nL - k0);
+    const long long E0 = A.elim_ptr[rs + k0];
+    int c = 0, d = 0;
+    long long e1 = 0;
+    if (hl < kc0) {
+      c = H.col[k0 + hl];
+      d = A.diag[c];
+      e1 = A.elim_ptr[rs + k0 + hl + 1];
+    }
+    // the chunk: the leading pivots whose ops fit the half's list
+    const bool fit = hl < kc0 && e1 - E0 <= kPairOps;
+    const int kc = __popc(__ballot_sync(hmask, fit));
+    if (hl < kc) {
+      H.opend[hl] = (int)(e1 - E0);
+      H.pivc[hl] = c;
+    }
+    const int nops = (int)(__shfl_sync(hmask, e1, kc - 1, 16) - E0);
+    for (int o = hl; o < nops; o += 16) {
+      const int2 op = __ldg(A.elim + E0 + o);
+      H.opq[o] = op.x;
+      H.opw[o] = op.y;
+    }
+    __syncwarp(hmask);
+    // every probe of the chunk in flight before any is checked
+    double dv = 0.0;
+    bool dmiss = false;
+    {
+      Probe pd{0, 0};
+      const bool have = hl < kc;
+      if (have && c < A.ready_below) dv = __ldcg(A.val + d);
+      else if (have) pd = probe_issue(A.mbox, d);
+      Probe po[kSlots];
+      bool old[kSlots];
+#pragma unroll
+      for (int i = 0; i < kSlots; ++i) {
+        const int o = i * 16 + hl;
+        po[i] = Probe{0, 0};
+        old[i] = false;
+        if (o < nops) {
+          if (A.ready_below > 0) {
+            int lo = 0, hi = kc - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (H.opend[mid] > o) hi = mid; else lo = mid + 1;
+            }
+            old[i] = H.pivc[lo] < A.ready_below;
+          }
+          if (old[i]) H.opv[o] = __ldcg(A.val + H.opq[o]);
+          else po[i] = probe_issue(A.mbox, H.opq[o]);
+        }
+      }
+      if (have && c >= A.ready_below) {
+        if (probe_ok(pd, A.epoch)) dv = probe_val(pd);
+        else dmiss = true;
+      }
+      unsigned omiss = 0;
+#pragma unroll
+      for (int i = 0; i < kSlots; ++i) {
+        const int o = i * 16 + hl;
+        if (o < nops && !old[i]) {
+          if (probe_ok(po[i], A.epoch)) H.opv[o] = probe_val(po[i]);
+          else omiss |= 1u << i;
+        }
+      }
+      if (__any_sync(hmask, dmiss)) {
+        const double v = half_value(A, dmiss, d, hmask);
+        if (dmiss) dv = v;
+      }
+      if (__any_sync(hmask, omiss != 0)) {
+        for (int i = 0; i < kSlots; ++i) {
+          const bool m = (omiss >> i) & 1;
+          const double v = half_value(A, m, m ? H.opq[i * 16 + hl] : 0, hmask);
+          if (m) H.opv[i * 16 + hl] = v;
+        }
+      }
+    }
+    __syncwarp(hmask);
+    // elimination, pivot by pivot
+    for (int kk = 0, o0 = 0; kk < kc; ++kk) {
+      const int k = k0 + kk;
+      const int o1 = H.opend[kk];
+      const double dk = __shfl_sync(hmask, dv, kk, 16);
+      double l = 0.0;
+      int drop = 0;
+      if (hl == 0) {
+        bool slow;
+        const double a = av[k];
+        l = jv::ddiv_fast(a, dk, slow);
+        if (slow) l = __ddiv_rn(a, dk);
+        drop = A.tau > 0.0 && fabs(l) < thresh;
+        av[k] = drop ? 0.0 : l;
+      }
+      l = __shfl_sync(hmask, l, 0, 16);
+      drop = __shfl_sync(hmask, drop, 0, 16);
+      if (A.milu) {
+        if (hl == 0)
+          for (int o = o0; o < o1; ++o) {
+            const int t = (drop || (H.opw[o] & kOut)) ? nL : H.opw[o];
+            av[t] = jv::dsub(av[t], jv::dmul(l, H.opv[o]));
+          }
+      } else if (!drop) {
+        for (int o = o0 + hl; o < o1; o += 16) {
+          const int t = H.opw[o];
+          av[t] = jv::dsub(av[t], jv::dmul(l, H.opv[o]));
+        }
+      }
+      o0 = o1;
+      __syncwarp(hmask);
+    }
+    k0 += kc;
+  }
+  for (int i = hl; i < len; i += 16) {
+    const double v = av[i];
+    __stcg(A.val + rs + i, v);
+    if (i >= nL) jv::mbox_put(A.mbox, rs + i, v, A.epoch);
+  }
+  if (hl == 0 && av[nL] == 0.0) atomicMin(A.err, r);
+  __syncwarp(hmask);
+}
+
 // Apply all pivots of row r with the whole warp.
 JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W, const jv::Trace& T,
                         int bt) {
@@ -562,7 +742,7 @@ JV_INLINE void warp_row(const FactorArgs& A, int r, int lane, WarpArena& W, cons
   const int dloc = A.diag[r] - rs;
   const int nL = dloc;
   const bool cached = len <= kWarpRow;
-  const bool listed = A.heavy != nullptr && A.heavy[r] == 1;
+  const bool listed = A.heavy != nullptr && (A.heavy[r] == 1 || A.heavy[r] == 3);
   double* av = cached ? W.val : A.val + rs;
   const int* ac = cached ? W.col : A.col + rs;
   if (cached) {
@@ -1162,6 +1342,8 @@ JV_INLINE void heavy_row(const FactorArgs& A, int r, int lane, int* heavy_busy, 
 constexpr size_t kFactorSmem = kArenaBytes + kSliceBytes + sizeof(double) * kHeavyCap;
 static_assert(kFactorSmem <= 232448 - 64, "factor kernel shared memory");
 
+static_assert(2 * sizeof(HalfArena) <= 32 * kSlotsD * sizeof(double), "pair arenas must fit a slice block");
+
 __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
 
   const unsigned full = 0xffffffffu;
@@ -1181,11 +1363,26 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
     const int idx = lo + lane;
     const bool active = idx < hi;
     const int r = active ? A.order[idx] : -1;
+    // batch class from the schedule (loaded alongside batch_ptr)
+    const int bcls = A.bclass != nullptr ? A.bclass[b] : -1;
     if (lane == 0) jv::trace_mark(T, b, 1);
+    // row flags (jv_elim_lists): 0 thread path, 1 pairable listed warp row,
+    // 2 heavy, 3 listed warp row
+    const int flag = (bcls != 0 && A.heavy != nullptr && active) ? A.heavy[r] : 0;
+    if (bcls == 1 && hi - lo == 2 && __shfl_sync(full, flag, 0) == 1 &&
+        __shfl_sync(full, flag, 1) == 1) {
+      const int half = lane >> 4;
+      const unsigned hmask = 0xffffu << (16 * half);
+      HalfArena* HA = reinterpret_cast<HalfArena*>(slice_doubles(threadIdx.x >> 5));
+      pair_row(A, __shfl_sync(full, r, half), lane & 15, hmask, HA[half]);
+      __syncwarp();
+      if (lane == 0) jv::trace_mark(T, b, 4);
+      continue;
+    }
     SfpRow F;
     ShortRow R;
     bool sfp = false, fits = false;
-    if (active) {
+    if (active && flag == 0) {
       sfp = sfp_structure(A, r, F);
       if (!sfp) fits = short_structure(A, r, R, S);
     }
@@ -1249,7 +1446,7 @@ extern "C" int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col
                          const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
                          int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
                          int32_t* ticket, const int8_t* heavy, const int64_t* elim_ptr,
-                         const int32_t* elim, void* stream) {
+                         const int32_t* elim, const int8_t* batch_class, void* stream) {
   if (n < 0 || nbatch < 0 || epoch == 0) {
     jvh::set_error("jv_factor: bad argument (n=%d nbatch=%d epoch=%u)", n, nbatch, epoch);
     return JV_EINVAL;
@@ -1257,7 +1454,8 @@ extern "C" int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col
   if (n == 0 || nbatch == 0) return JV_OK;
   FactorArgs A{row_start, col, val, diag_pos, norms, tau, milu, order, batch_ptr,
                nbatch, ready_below, mbox, epoch, err_row, ticket,
-               elim != nullptr ? heavy : nullptr, elim_ptr, reinterpret_cast<const int2*>(elim)};
+               elim != nullptr ? heavy : nullptr, elim_ptr, reinterpret_cast<const int2*>(elim),
+               batch_class};
   void* args[] = {&A};
   return jvh::persistent_launch(factor_kernel, kThreads, args, (cudaStream_t)stream, "jv_factor",
                                 kFactorSmem);

@@ -166,17 +166,24 @@ __global__ void batch_fill_kernel(int nlev, const int32_t* level_ptr, const int3
 
 // class-aware schedule: groups = (level, class) in key order (key = 2*level
 // + class); class 0 rows are cut into batches of 32, class 1 rows one each
-__global__ void group_batch_count_kernel(int ngroups, const int32_t* gptr, int32_t* cnt) {
+// batch size per row class: key = nclass * level + class
+struct BatchSteps {
+  int nclass;
+  int step[4];
+};
+__global__ void group_batch_count_kernel(int ngroups, const int32_t* gptr, BatchSteps bs,
+                                         int32_t* cnt) {
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
     const int c = gptr[g + 1] - gptr[g];
-    cnt[g] = (g & 1) ? c : (c + 31) / 32;
+    const int st = bs.step[g % bs.nclass];
+    cnt[g] = (c + st - 1) / st;
   }
 }
 __global__ void group_batch_fill_kernel(int ngroups, const int32_t* gptr, const int32_t* boff,
-                                        int32_t* batch_ptr, int m) {
+                                        BatchSteps bs, int32_t* batch_ptr, int m) {
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
     const int a = gptr[g], b = gptr[g + 1];
-    const int step = (g & 1) ? 1 : 32;
+    const int step = bs.step[g % bs.nclass];
     int o = boff[g];
     for (int s = a; s < b; s += step) batch_ptr[o++] = s;
   }
@@ -700,11 +707,20 @@ extern "C" int jv_row_norms(int32_t n, const int32_t* row_start, const double* v
   return JV_OK;
 }
 
-extern "C" int jv_build_schedule(int32_t m, const int32_t* rows, const int32_t* keys, int32_t nkeys,
-                                 int32_t* order, int32_t* batch_ptr, int32_t* nbatch_h,
-                                 void* stream) {
+extern "C" int jv_build_schedule_n(int32_t m, const int32_t* rows, const int32_t* keys,
+                                   int32_t nkeys, int32_t nclass, const int32_t* steps,
+                                   int32_t* order, int32_t* batch_ptr, int32_t* nbatch_h,
+                                   void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (m < 0 || nkeys < 0) { jvh::set_error("jv_build_schedule: bad argument"); return JV_EINVAL; }
+  if (m < 0 || nkeys < 0 || nclass < 1 || nclass > 4) {
+    jvh::set_error("jv_build_schedule: bad argument");
+    return JV_EINVAL;
+  }
+  BatchSteps bs{nclass, {1, 1, 1, 1}};
+  for (int c = 0; c < nclass; ++c) {
+    if (steps[c] < 1) { jvh::set_error("jv_build_schedule: step < 1"); return JV_EINVAL; }
+    bs.step[c] = steps[c];
+  }
   if (m == 0) {
     set_int_kernel<<<1, 1, 0, s>>>(batch_ptr, 0);
     *nbatch_h = 0;
@@ -733,12 +749,12 @@ extern "C" int jv_build_schedule(int32_t m, const int32_t* rows, const int32_t* 
   level_ptr_kernel<<<grid_for(m), kSetupThreads, 0, s>>>(m, nkeys, (const int32_t*)skeys.p,
                                                          (int32_t*)gptr.p);
   group_batch_count_kernel<<<grid_for(nkeys), kSetupThreads, 0, s>>>(nkeys, (const int32_t*)gptr.p,
-                                                                     (int32_t*)cnt.p);
+                                                                     bs, (int32_t*)cnt.p);
   set_int_kernel<<<1, 1, 0, s>>>((int32_t*)cnt.p + nkeys, 0);
   CK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, (int32_t*)cnt.p, (int32_t*)off.p, nkeys + 1, s),
           "scan");
   group_batch_fill_kernel<<<grid_for(nkeys), kSetupThreads, 0, s>>>(
-      nkeys, (const int32_t*)gptr.p, (const int32_t*)off.p, batch_ptr, m);
+      nkeys, (const int32_t*)gptr.p, (const int32_t*)off.p, bs, batch_ptr, m);
   JV_CHECK_LAUNCH("jv_build_schedule");
   int32_t nb = 0;
   CK_CUDA(cudaMemcpyAsync(&nb, (int32_t*)off.p + nkeys, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
@@ -746,4 +762,11 @@ extern "C" int jv_build_schedule(int32_t m, const int32_t* rows, const int32_t* 
   CK_CUDA(cudaStreamSynchronize(s), "sync");
   *nbatch_h = nb;
   return JV_OK;
+}
+
+extern "C" int jv_build_schedule(int32_t m, const int32_t* rows, const int32_t* keys, int32_t nkeys,
+                                 int32_t* order, int32_t* batch_ptr, int32_t* nbatch_h,
+                                 void* stream) {
+  const int32_t steps[2] = {32, 1};
+  return jv_build_schedule_n(m, rows, keys, nkeys, 2, steps, order, batch_ptr, nbatch_h, stream);
 }

@@ -264,43 +264,59 @@ def batches_dev(nlev, level_ptr, n):
 
 @dataclass
 class Schedule:
-    """Level-batched row order for a sync-free sweep (jv_build_schedule):
-    keys = 2*level + class; class 0 rows 32 per batch, class 1 one each."""
+    """Level-batched row order for a sync-free sweep (jv_build_schedule_n):
+    keys = nclass*level + class; class c rows steps[c] per batch."""
 
     order: object
     batch_ptr: object
     nbatch: int
     nkeys: int
     keys: object = None      # per-row key (indexed by row id)
+    steps: tuple = (32, 1)
 
     def restrict(self, lo, hi):
         """Rows with lo <= index < hi, keeping level order and classes."""
         t = torch()
         rows = t.arange(lo, hi, dtype=t.int32, device="cuda")
         keys = self.keys[lo:hi].contiguous()
-        return build_schedule(rows, keys, self.nkeys)
+        sub = build_schedule(rows, keys, self.nkeys, self.steps)
+        sub.keys = self.keys
+        return sub
+
+    def batch_class(self):
+        """int8 class of every batch (key % nclass of its first row)."""
+        if getattr(self, "_bclass", None) is None:
+            t = torch()
+            first = self.order[self.batch_ptr[:self.nbatch].long()].long()
+            self._bclass = (self.keys[first] % len(self.steps)).to(t.int8).contiguous()
+        return self._bclass
 
 
-def build_schedule(rows, keys, nkeys):
+def build_schedule(rows, keys, nkeys, steps=(32, 1)):
     m = int(keys.numel())
     order = empty_i32(m)
     batch_ptr = empty_i32(m + nkeys + 2)
     nb = ctypes.c_int32(0)
-    _lib.call("jv_build_schedule", m, ptr(rows), ptr(keys), int(nkeys), ptr(order),
-              ptr(batch_ptr), ctypes.byref(nb), stream())
-    return Schedule(order, batch_ptr, int(nb.value), nkeys)
+    st = (ctypes.c_int32 * len(steps))(*steps)
+    _lib.call("jv_build_schedule_n", m, ptr(rows), ptr(keys), int(nkeys), len(steps), st,
+              ptr(order), ptr(batch_ptr), ctypes.byref(nb), stream())
+    return Schedule(order, batch_ptr, int(nb.value), nkeys, None, tuple(steps))
 
 
-def schedule_dev(a: DevCsr, backward: bool, cls=None):
+def schedule_dev(a: DevCsr, backward: bool, cls=None, steps=(32, 1), level_of=None):
     """Schedule of a sweep over pattern `a`: its levels (forward: columns <
-    r, backward: columns > r) plus per-row classes (None = all thread path)."""
+    r, backward: columns > r) plus per-row classes (None = all class 0)."""
     t = torch()
-    level_of, nlev = levels_dev(a, backward)
-    keys = level_of.to(t.int32) * 2
+    if level_of is None:
+        level_of, nlev = levels_dev(a, backward)
+    else:
+        nlev = int(level_of.max().item()) + 1 if level_of.numel() else 0
+    nclass = len(steps)
+    keys = level_of.to(t.int32) * nclass
     if cls is not None:
         keys = keys + cls
     keys = keys.contiguous()
-    sched = build_schedule(None, keys, 2 * max(nlev, 1))
+    sched = build_schedule(None, keys, nclass * max(nlev, 1), steps)
     sched.keys = keys
     return sched, level_of
 
@@ -346,6 +362,12 @@ class DevIlu:
                       tau, milu)
 
     # schedules --------------------------------------------------------
+    def _factor_classes(self):
+        key = bool(self.milu)
+        if getattr(self, "_fcls", None) is None or self._fcls[0] != key:
+            self._fcls = (key, self._classes("factor"))
+        return self._fcls[1]
+
     def _classes(self, kind):
         cls = empty_i32(self.n)
         if kind == "factor":
@@ -357,9 +379,24 @@ class DevIlu:
         return cls
 
     def factor_schedule(self):
+        """Factor sweep schedule: thread-path rows 32 to a batch, pairable
+        listed warp rows (jv_elim_lists flag 1) two to a batch, other warp
+        rows one to a batch."""
         if self._fsched is None or self._fsched_milu != self.milu:
+            t = torch()
+            cls = self._factor_classes()
+            el = self.elim_lists()
+            cls3 = cls
+            if el is not None:
+                flags = el[0][:self.n].to(t.int32)
+                cls3 = t.where(cls == 0, t.zeros_like(cls),
+                               t.where(flags == 1, t.ones_like(cls), t.full_like(cls, 2)))
+            else:
+                cls3 = cls * 2
             self._fsched, self._fwd_levels = schedule_dev(self.pattern, False,
-                                                          self._classes("factor"))
+                                                          cls3.to(t.int32).contiguous(),
+                                                          steps=(32, 2, 1),
+                                                          level_of=self._fwd_levels)
             self._fsched_milu = self.milu
         return self._fsched
 
@@ -376,7 +413,7 @@ class DevIlu:
             eptr = t.empty(self.nnz + 1, dtype=t.int64, device="cuda")
             nops = ctypes.c_int64(0)
             args = [self.n, ptr(self.row_start), ptr(self.col), ptr(self.diag_pos), int(self.milu),
-                    self.ELIM_MIN_CAND, ptr(self._classes("factor")) if self.ELIM_WARP_ROWS else None,
+                    self.ELIM_MIN_CAND, ptr(self._factor_classes()) if self.ELIM_WARP_ROWS else None,
                     ptr(heavy), ptr(eptr)]
             _lib.call("jv_elim_lists", *args, None, ctypes.byref(nops), stream())
             lists = None
@@ -498,7 +535,8 @@ class DevIlu:
                   ptr(sched.batch_ptr), sched.nbatch, int(ready_below), ptr(self.fbox.buf),
                   self.fbox.next_epoch(), ptr(self.err), ptr(self.ticket),
                   ptr(el[0]) if el else None, ptr(el[1]) if el else None,
-                  ptr(el[2]) if el else None, stream())
+                  ptr(el[2]) if el else None,
+                  ptr(sched.batch_class()) if sched.nbatch else None, stream())
 
     def factor(self, lo=0, hi=None, ready_below=0):
         """Factor and return the smallest zero-pivot row (or -1)."""

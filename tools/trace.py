@@ -62,8 +62,9 @@ def main():
                         rs=dv.host_i64(ilu.row_start, ilu.n + 1), diag=dv.host_i64(ilu.diag_pos, ilu.n),
                         heavy=(ilu.elim_lists()[0][:ilu.n].cpu().numpy() if ilu.elim_lists()
                                else np.zeros(ilu.n, np.int8)))
-    lev = keys[first] // 2
-    cls = keys[first] % 2
+    ncls = len(getattr(sch, "steps", (32, 1)))
+    lev = keys[first] // ncls
+    cls = keys[first] % ncls
     t = tr[:, :5] - tr[:, 0].min()
     nlev = int(lev.max()) + 1
     lev_end = np.array([t[lev == L, 4].max() for L in range(nlev)])
