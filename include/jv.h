@@ -161,6 +161,14 @@ int jv_rcm_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h, int
 int64_t jv_iluk_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h, int32_t k,
                      int32_t** out_row_start_h, int32_t** out_col_h, int32_t** out_lev_h);
 void jv_free_host(void* p);
+/* Hub-row gather plan (host; see host.cpp): the target-parallel schedule of
+ * one heavy row's elimination list (piv_ptr[nL+1] absolute offsets of each
+ * pivot's ops, op_q/op_w indexed from piv_ptr[0]; dslot[nL] = mailbox slot
+ * of each pivot's diagonal).  stream: int32[2*(nops + nL)], meta:
+ * int32[1 + 33*(nL + 2)] upper bounds; returns 0 or -1.                  */
+int jv_hub_plan_host(int32_t len, int32_t nL, const int64_t* piv_ptr, const int32_t* op_q,
+                     const int32_t* op_w, const int32_t* dslot, int32_t* stream,
+                     int64_t* nstream, int32_t* meta, int64_t* nmeta);
 
 /* ---- numeric factorization ------------------------------------------
  * Sync-free up-looking ILU(k,tau) over rows taken in `order` (a
@@ -179,7 +187,13 @@ int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col, double* v
               const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
               int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
               int32_t* ticket, const int8_t* heavy, const int64_t* elim_ptr,
-              const int32_t* elim, const int8_t* batch_class, void* stream);
+              const int32_t* elim, const int8_t* batch_class, const int32_t* hub_stream,
+              const int64_t* hub_sptr, const int32_t* hub_meta, const int64_t* hub_mptr,
+              void* stream);
+/* hub_* (nullable): gather plans of the rows flagged 4 in `heavy`
+ * (jv_hub_plan_host, concatenated): hub_sptr[r] / hub_mptr[r] = offsets of
+ * row r's stream entries (int2) and meta.  Used for full factorizations
+ * with tau = 0 and no MILU; otherwise those rows take the heavy path.     */
 /* batch_class (nullable): class of each batch of the schedule (0: up to 32
  * thread-path rows, 1: a pair of listed warp rows, 2: one warp row), i.e.
  * key % 3 of its first row under jv_build_schedule_n(nclass 3).          */

@@ -54,12 +54,14 @@ _SIGS = {
     "jv_iluk_host": [c_int32, _P, _P, c_int32, POINTER(_I32P), POINTER(_I32P), POINTER(_I32P)],
     "jv_free_host": [c_void_p],
     "jv_factor": [c_int32, _P, _P, _P, _P, _P, c_double, c_int, _P, _P, c_int32, c_int32, _P,
-                  c_uint32, _P, _P, _P, _P, _P, _P, _P],
+                  c_uint32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "jv_elim_lists": [c_int32, _P, _P, _P, c_int, c_int64, _P, _P, _P, _P, POINTER(c_int64), _P],
     "jv_solve": [c_int, c_int32, _P, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, c_uint32, _P, _P],
     "jv_check_zero_diag": [c_int32, _P, _P, _P, _P],
     "jv_build_batches": [c_int32, _P, _P, _I32P, _P],
     "jv_build_schedule": [c_int32, _P, _P, c_int32, _P, _P, _I32P, _P],
+    "jv_hub_plan_host": [c_int32, c_int32, _P, _P, _P, _P, _P, POINTER(c_int64), _P,
+                         POINTER(c_int64)],
     "jv_build_schedule_n": [c_int32, _P, _P, c_int32, c_int32, _P, _P, _P, _I32P, _P],
     "jv_classify_factor": [c_int32, _P, _P, _P, c_int, _P, _P],
     "jv_classify_solve": [c_int, c_int32, _P, _P, _P, _P],

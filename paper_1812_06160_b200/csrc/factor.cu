@@ -79,6 +79,10 @@ struct FactorArgs {
   const int64_t* elim_ptr;    // [nnz+1]: ops of L entry p = [elim_ptr[p], elim_ptr[p+1])
   const int2* elim;           // op = (q: U entry of the pivot row, w: target position | kOut)
   const int8_t* bclass;       // nullable: batch class (0 thread rows, 1 row pair, 2 single row)
+  const int2* hub_stream;     // nullable: hub-row gather plans (jv_hub_plan_host)
+  const int64_t* hub_sptr;    // per row: first stream entry (rows with flag 4)
+  const int32_t* hub_meta;
+  const int64_t* hub_mptr;    // per row: offset of [nphases, 32 lane loads per phase]
 };
 
 struct WarpArena {
@@ -1097,7 +1101,7 @@ struct HeavyStream {
 #pragma unroll
     for (int h = 0; h < kWin; h += 32) {
       const int e = i * kWin + h + lane;
-      if (e < nops) cp_async16(R.pkt(e), mbox + 2 * (long long)R.op(e)->x);
+      if (e < nops) cp_async16(R.pkt(e), mbox + 2 * (long long)(R.op(e)->x & 0x7fffffff));
     }
     cp_commit();
   }
@@ -1339,6 +1343,197 @@ JV_INLINE void heavy_row(const FactorArgs& A, int r, int lane, int* heavy_busy, 
 #endif
 }
 
+// Hub rows with a gather plan (flag 4, jv_hub_plan_host): instead of the
+// pivot-by-pivot walk, positions are folded in parallel — phase by phase
+// (in-row dependency depth), each lane running its queue of (position,
+// update run) items from a step-major stream that the same cp.async ring
+// prefetches (update entries and their mailbox packets alike).  Bitwise
+// equal to the pivot order: every position still receives its updates in
+// ascending pivot order (tests/test_hubplan.py replays plans on the CPU).
+// Needs the CTA row buffer; returns false (caller falls back to heavy_row)
+// when the buffer is taken or the row does not fit.
+JV_INLINE bool hub_row(const FactorArgs& A, int r, int lane, int* heavy_busy, double* hbuf,
+                       const jv::Trace& T, int bt) {
+  [[maybe_unused]] long long hp_adv = 0, hp_miss = 0, hp_divb = 0, hp_steps = 0;
+  HP_T0(hp_start);
+  const unsigned full = 0xffffffffu;
+  const int rs = A.row_start[r], re = A.row_start[r + 1];
+  const int len = re - rs;
+  const int nL = A.diag[r] - rs;
+  int bits = 0;
+  if (lane == 0 && len <= kHeavyCap) {
+    for (int tries = 0; tries < 4 && !bits; ++tries) {
+      const int st = *reinterpret_cast<volatile int*>(heavy_busy);
+      int want = 0;
+      if (len > kHeavyCap / 2) want = st == 0 ? 3 : 0;
+      else if (!(st & 1)) want = 1;
+      else if (!(st & 2)) want = 2;
+      if (!want) break;
+      if (atomicCAS(heavy_busy, st, st | want) == st) bits = want;
+    }
+  }
+  bits = __shfl_sync(full, bits, 0);
+  if (!bits) return false;
+  double* av = hbuf + (bits == 2 ? kHeavyCap / 2 : 0);
+  for (int i = lane; i < len; i += 32) av[i] = __ldcg(A.val + rs + i);
+
+  const long long s0 = A.hub_sptr[r];
+  const int32_t* meta = A.hub_meta + A.hub_mptr[r];
+  const int nph = meta[0];
+  HeavyStream H;
+  H.elim = A.hub_stream;
+  H.mbox = A.mbox;
+  H.R.ops = reinterpret_cast<int2*>(slice_ints(threadIdx.x >> 5));
+  H.R.pkts = reinterpret_cast<uint64_t*>(slice_doubles(threadIdx.x >> 5));
+  H.O0 = s0;
+  H.lane = lane;
+  // entries of the row: every phase's lane loads plus its divisions
+  {
+    long long tot = 0;
+    for (int p = 0; p < nph; ++p) tot += meta[1 + 33 * p + lane] + (lane == 0 ? meta[33 * p + 33] : 0);
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(full, tot, o);
+    H.nops = (int)tot;
+  }
+  __syncwarp();
+  H.prologue();
+  int cur = 0;
+  H.advance(0);
+
+  int qnext = nph > 0 ? meta[1 + lane] : 0;
+  int fnext = nph > 0 ? meta[33] : 0;
+  int base = 0;
+  for (int p = 0; p < nph; ++p) {
+    const int qlen = qnext, nfin = fnext;
+    if (p + 1 < nph) {
+      qnext = meta[1 + 33 * (p + 1) + lane];
+      fnext = meta[33 * (p + 1) + 33];
+    }
+    const int maxq = __shfl_sync(full, qlen, 0);
+    // ---- update block: runs of independent positions, one fold per lane,
+    // four steps per round (their loads are independent: only the folds
+    // chain), so a single warp keeps several shared-memory loads in flight
+    int cw = -1;
+    double acc = 0.0;
+    constexpr int kU4 = 4;
+    for (int t0 = 0; t0 < maxq; t0 += kU4) {
+      int a[kU4], e[kU4];
+      int tot = 0;
+#pragma unroll
+      for (int i = 0; i < kU4; ++i) {
+        const bool act = t0 + i < qlen;
+        a[i] = __popc(__ballot_sync(full, t0 + i < maxq ? act : false));
+        e[i] = act ? base + tot + lane : -1;
+        tot += a[i];
+      }
+      HP_T0(t_adv);
+      if (tot > 0) {
+        const int need = (base + tot - 1) / kWin;
+        while (cur < need) H.advance(++cur);
+      }
+      HP_ADD(hp_adv, t_adv);
+#ifdef JV_HEAVY_PROFILE
+      hp_steps += kU4;
+#endif
+      int2 op[kU4];
+      double u[kU4], lj[kU4];
+      unsigned missm = 0;
+#pragma unroll
+      for (int i = 0; i < kU4; ++i) {
+        op[i] = make_int2(0, 0);
+        u[i] = 0.0;
+        if (e[i] >= 0) {
+          op[i] = *H.R.op(e[i]);
+          const ulonglong2 pk = *reinterpret_cast<const ulonglong2*>(H.R.pkt(e[i]));
+          u[i] = __longlong_as_double((long long)((pk.x & 0xffffffffull) | (pk.y << 32)));
+          if ((uint32_t)(pk.x >> 32) != A.epoch || (uint32_t)(pk.y >> 32) != A.epoch)
+            missm |= 1u << i;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kU4; ++i) lj[i] = e[i] >= 0 ? av[op[i].y & 0xffff] : 0.0;
+      if (__any_sync(full, missm != 0)) {
+        HP_T0(t_miss);
+        for (int i = 0; i < kU4; ++i) {
+          const bool m = (missm >> i) & 1;
+          const double v = warp_value(A, m, 0, op[i].x);
+          if (m) u[i] = v;
+        }
+        HP_ADD(hp_miss, t_miss);
+      }
+#pragma unroll
+      for (int i = 0; i < kU4; ++i) {
+        if (e[i] >= 0) {
+          const int w = (int)((unsigned)op[i].y >> 16);
+          if (w != cw) {
+            if (cw >= 0) av[cw] = acc;
+            cw = w;
+            acc = av[w];
+          }
+          acc = jv::dsub(acc, jv::dmul(lj[i], u[i]));
+        }
+      }
+      base += tot;
+    }
+    if (cw >= 0) av[cw] = acc;
+    __syncwarp();
+    // ---- division block: the L positions of this depth
+    HP_T0(t_divb);
+    for (int f0 = 0; f0 < nfin; f0 += 32) {
+      const int a = min(32, nfin - f0);
+      const int need = (base + a - 1) / kWin;
+      while (cur < need) H.advance(++cur);
+      int w = 0, x = 0;
+      double d = 1.0;
+      bool miss = false;
+      if (lane < a) {
+        const int e = base + lane;
+        const int2 op = *H.R.op(e);
+        x = op.x & 0x7fffffff;
+        w = (int)((unsigned)op.y >> 16);
+        const ulonglong2 pk = *reinterpret_cast<const ulonglong2*>(H.R.pkt(e));
+        d = __longlong_as_double((long long)((pk.x & 0xffffffffull) | (pk.y << 32)));
+        miss = (uint32_t)(pk.x >> 32) != A.epoch || (uint32_t)(pk.y >> 32) != A.epoch;
+      }
+      if (__any_sync(full, miss)) {
+        const double v = warp_value(A, miss, 0, x);
+        if (miss) d = v;
+      }
+      if (lane < a) {
+        const double num = av[w];
+        bool slow;
+        double l = jv::ddiv_fast(num, d, slow);
+        if (slow) l = __ddiv_rn(num, d);
+        av[w] = l;
+      }
+      base += a;
+    }
+    HP_ADD(hp_divb, t_divb);
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __syncwarp();
+  for (int i = lane; i < len; i += 32) {
+    const double v = av[i];
+    __stcg(A.val + rs + i, v);
+    if (i >= nL) jv::mbox_put(A.mbox, rs + i, v, A.epoch);
+  }
+  if (lane == 0 && av[nL] == 0.0) atomicMin(A.err, r);
+  __syncwarp();
+  if (lane == 0) atomicAnd(heavy_busy, ~bits);
+  __syncwarp();
+#ifdef JV_HEAVY_PROFILE
+  if (lane == 0) {
+    jv::trace_word(T, bt, 7, ((unsigned long long)hp_steps << 1) | 1);
+    jv::trace_word(T, bt, 13, hp_adv);
+    jv::trace_word(T, bt, 14, hp_miss);
+    jv::trace_word(T, bt, 15, ((unsigned long long)hp_divb << 32) | (unsigned)(clock64() - hp_start));
+  }
+#else
+  (void)T; (void)bt;
+#endif
+  return true;
+}
+
 constexpr size_t kFactorSmem = kArenaBytes + kSliceBytes + sizeof(double) * kHeavyCap;
 static_assert(kFactorSmem <= 232448 - 64, "factor kernel shared memory");
 
@@ -1408,7 +1603,10 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
       const int rr = __shfl_sync(full, r, src);
-      if (A.heavy != nullptr && A.heavy[rr] == 2) heavy_row(A, rr, lane, &heavy_busy, hbuf, T, b);
+      const int fl = A.heavy != nullptr ? A.heavy[rr] : 0;
+      if (fl == 4 && A.ready_below == 0 && !A.milu && A.tau == 0.0 &&
+          hub_row(A, rr, lane, &heavy_busy, hbuf, T, b)) {
+      } else if (fl == 2 || fl == 4) heavy_row(A, rr, lane, &heavy_busy, hbuf, T, b);
       else warp_row(A, rr, lane, W, T, b);
     }
     __syncwarp();
@@ -1446,7 +1644,9 @@ extern "C" int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col
                          const int32_t* order, const int32_t* batch_ptr, int32_t nbatch,
                          int32_t ready_below, uint64_t* mbox, uint32_t epoch, int32_t* err_row,
                          int32_t* ticket, const int8_t* heavy, const int64_t* elim_ptr,
-                         const int32_t* elim, const int8_t* batch_class, void* stream) {
+                         const int32_t* elim, const int8_t* batch_class,
+                         const int32_t* hub_stream, const int64_t* hub_sptr,
+                         const int32_t* hub_meta, const int64_t* hub_mptr, void* stream) {
   if (n < 0 || nbatch < 0 || epoch == 0) {
     jvh::set_error("jv_factor: bad argument (n=%d nbatch=%d epoch=%u)", n, nbatch, epoch);
     return JV_EINVAL;
@@ -1455,7 +1655,8 @@ extern "C" int jv_factor(int32_t n, const int32_t* row_start, const int32_t* col
   FactorArgs A{row_start, col, val, diag_pos, norms, tau, milu, order, batch_ptr,
                nbatch, ready_below, mbox, epoch, err_row, ticket,
                elim != nullptr ? heavy : nullptr, elim_ptr, reinterpret_cast<const int2*>(elim),
-               batch_class};
+               batch_class, reinterpret_cast<const int2*>(hub_stream), hub_sptr, hub_meta,
+               hub_mptr};
   void* args[] = {&A};
   return jvh::persistent_launch(factor_kernel, kThreads, args, (cudaStream_t)stream, "jv_factor",
                                 kFactorSmem);

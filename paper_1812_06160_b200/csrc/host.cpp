@@ -342,3 +342,138 @@ extern "C" int64_t jv_region_desc_host(int32_t n, const int32_t* rs, const int32
   }
   return bad;
 }
+
+// ---------------------------------------------------------------------------
+// Hub-row gather plan (setup, host): the target-parallel schedule of one
+// heavy row's elimination, so the numeric kernel folds many positions at
+// once instead of walking the pivots one by one.
+//
+// Input: the row's elimination list in pivot order (jv_elim_lists): pivot j
+// owns ops [piv_ptr[j], piv_ptr[j+1]) = (q, w): subtract l_j * u_q from
+// position w.  For every position w the updates must be applied in
+// ascending j (the order of _factor_row, _kernels.py:165-194), and l_w
+// (w < nL) = (a_w - its updates) / d_w is available to later updates.
+//
+//   depth(w) = 1 + max depth(j) over w's updaters (0 without any), w < nL;
+//   an update (j -> w) can run in phase depth(j) + 1, and not before the
+//   previous update of w  ->  each position's updates split into runs, one
+//   per phase; an L position w is finalised (divided) in phase depth(w).
+//   Phases run in order; inside a phase, runs of different positions are
+//   independent and are dealt to 32 lanes longest-first (LPT), lanes sorted
+//   by load, and the stream is step-major (step t: entry t of every lane
+//   with more than t entries), so lanes t < active(t) are a prefix.  The
+//   phase's divisions follow as a block of their own (32 per step), after
+//   every update of the phase: no division diverges inside an update step.
+//
+// Stream entry (int2): x = q (update) or d_slot | 1<<31 (finalise: divide by
+// the pivot diagonal, mailbox slot d_slot); y = j | w << 16 (j unused for a
+// finalise).  Meta: nphases, then per phase 32 lane loads (descending) and
+// the number of divisions.
+// Returns 0, or -1 when a row does not fit (len > 65535).
+extern "C" int jv_hub_plan_host(int32_t len, int32_t nL, const int64_t* piv_ptr,
+                                const int32_t* op_q, const int32_t* op_w, const int32_t* dslot,
+                                int32_t* stream, int64_t* nstream, int32_t* meta, int64_t* nmeta) {
+  if (len > 65535 || nL > len) return -1;
+  const int64_t nops = piv_ptr[nL] - piv_ptr[0];
+  const int64_t base = piv_ptr[0];
+  for (int64_t o = 0; o < nops; ++o)
+    if (op_w[o] < 0 || op_w[o] >= len) return -1;   // e.g. MILU out-of-pattern targets
+  // 1. updates grouped by target, ascending pivot (counting sort, stable)
+  std::vector<int32_t> cnt(len + 1, 0);
+  for (int64_t o = 0; o < nops; ++o) cnt[op_w[o] + 1]++;
+  for (int w = 0; w < len; ++w) cnt[w + 1] += cnt[w];
+  std::vector<int32_t> gj(nops), gq(nops), fill(cnt.begin(), cnt.end() - 1);
+  for (int j = 0; j < nL; ++j)
+    for (int64_t o = piv_ptr[j] - base; o < piv_ptr[j + 1] - base; ++o) {
+      const int w = op_w[o];
+      gj[fill[w]] = j;
+      gq[fill[w]] = op_q[o];
+      fill[w]++;
+    }
+  // 2. in-row depth of the L positions
+  std::vector<int32_t> depth(nL, 0);
+  int D = -1;
+  for (int k = 0; k < nL; ++k) {
+    int d = -1;
+    for (int i = cnt[k]; i < cnt[k + 1]; ++i) d = std::max(d, depth[gj[i]]);
+    depth[k] = d + 1;
+    D = std::max(D, depth[k]);
+  }
+  const int P = D + 2;   // U positions may take updates up to phase D + 1
+  // 3. runs per phase: (w, first update, count, finalise)
+  struct Run { int32_t w, first, count; };
+  std::vector<std::vector<Run>> runs(P);
+  std::vector<std::vector<int32_t>> fins(P);
+  for (int w = 0; w < len; ++w) {
+    int ph = 0, start = cnt[w];
+    for (int i = cnt[w]; i < cnt[w + 1]; ++i) {
+      const int p = std::max(ph, depth[gj[i]] + 1);
+      if (p != ph && i > start) {
+        runs[ph].push_back({w, start, i - start});
+        start = i;
+      }
+      ph = p;
+    }
+    if (cnt[w + 1] > start) runs[ph].push_back({w, start, cnt[w + 1] - start});
+    // the last run sits in phase depth(w) (its newest updater has depth
+    // depth(w) - 1); the division follows in that phase's finalise block
+    if (w < nL) fins[depth[w]].push_back(w);
+  }
+  // 4. per phase: LPT over 32 lanes, lanes by load, step-major stream
+  int64_t ns = 0, nm = 0;
+  meta[nm++] = P;
+  std::vector<int32_t> order;
+  for (int p = 0; p < P; ++p) {
+    auto& rp = runs[p];
+    order.resize(rp.size());
+    for (size_t i = 0; i < rp.size(); ++i) order[i] = (int32_t)i;
+    auto cost = [&](const Run& r) { return r.count; };
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return cost(rp[a]) > cost(rp[b]); });
+    std::vector<std::vector<int32_t>> lane(32);
+    int64_t load[32] = {0};
+    for (int32_t i : order) {
+      int best = 0;
+      for (int l = 1; l < 32; ++l)
+        if (load[l] < load[best]) best = l;
+      lane[best].push_back(i);
+      load[best] += cost(rp[i]);
+    }
+    int perm[32];
+    for (int l = 0; l < 32; ++l) perm[l] = l;
+    std::stable_sort(perm, perm + 32, [&](int a, int b) { return load[a] > load[b]; });
+    // each lane's entry sequence
+    std::vector<std::vector<int64_t>> seq(32);   // packed (x << 32 | y)
+    for (int l = 0; l < 32; ++l) {
+      auto& s = seq[l];
+      for (int32_t i : lane[perm[l]]) {
+        const Run& r = rp[i];
+        for (int t = 0; t < r.count; ++t) {
+          const int g = r.first + t;
+          const uint32_t x = (uint32_t)gq[g];
+          const uint32_t y = (uint32_t)gj[g] | ((uint32_t)r.w << 16);
+          s.push_back((int64_t)(((uint64_t)x << 32) | y));
+        }
+      }
+      meta[nm++] = (int32_t)s.size();
+    }
+    const size_t steps = seq[0].size();
+    for (size_t t = 0; t < steps; ++t)
+      for (int l = 0; l < 32 && t < seq[l].size(); ++l) {
+        const uint64_t e = (uint64_t)seq[l][t];
+        stream[2 * ns] = (int32_t)(uint32_t)(e >> 32);
+        stream[2 * ns + 1] = (int32_t)(uint32_t)e;
+        ++ns;
+      }
+    // finalise block: the divisions of the phase, 32 per step
+    meta[nm++] = (int32_t)fins[p].size();
+    for (int32_t w : fins[p]) {
+      stream[2 * ns] = (int32_t)((uint32_t)dslot[w] | 0x80000000u);
+      stream[2 * ns + 1] = (int32_t)((uint32_t)w << 16);
+      ++ns;
+    }
+  }
+  *nstream = ns;
+  *nmeta = nm;
+  return 0;
+}

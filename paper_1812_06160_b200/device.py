@@ -424,6 +424,61 @@ class DevIlu:
             self._elim = (key, lists)
         return self._elim[1]
 
+    # hub rows: target-parallel gather plans (jv_hub_plan_host) for the
+    # heavy rows with at least HUB_MIN_OPS updates
+    HUB_MIN_OPS = 1024
+
+    def hub_plans(self):
+        """(stream, sptr, meta, mptr) device buffers or None; flags the
+        planned rows 4 in the elimination-list flags."""
+        el = self.elim_lists()
+        if el is None or self.milu:      # MILU lists carry out-of-pattern targets
+            return None
+        if getattr(self, "_hub", None) is not None and self._hub[0] is el:
+            return self._hub[1]
+        from concurrent.futures import ThreadPoolExecutor
+        from . import hubplan
+        t = torch()
+        n = self.n
+        flags_d, eptr_d, elim_d = el[0], el[1], el[2]
+        flags = flags_d[:n].cpu().numpy()
+        rs = host_i64(self.row_start, n + 1)
+        dg = host_i64(self.diag_pos, n)
+        cand = np.flatnonzero(flags == 2)
+        plans = None
+        if cand.size:
+            e_rs = eptr_d[t.from_numpy(rs[cand]).cuda()].cpu().numpy()
+            e_dg = eptr_d[t.from_numpy(dg[cand]).cuda()].cpu().numpy()
+            sel = cand[(e_dg - e_rs) >= self.HUB_MIN_OPS]
+            if sel.size:
+                def one(r):
+                    L = int(dg[r] - rs[r])
+                    piv = eptr_d[int(rs[r]):int(rs[r]) + L + 1].cpu().numpy()
+                    ops = elim_d[2 * int(piv[0]):2 * int(piv[-1])].cpu().numpy().reshape(-1, 2)
+                    cols = self.col[int(rs[r]):int(rs[r]) + L].long()
+                    dslot = self.diag_pos[cols].cpu().numpy()
+                    return hubplan.plan_row(int(rs[r + 1] - rs[r]), L, piv, ops[:, 0], ops[:, 1],
+                                            dslot)
+                with ThreadPoolExecutor(8) as ex:
+                    out = list(ex.map(one, sel))
+                keep = [(r, pl) for r, pl in zip(sel, out) if pl is not None]
+                if keep:
+                    sptr = np.full(n, -1, np.int64)
+                    mptr = np.full(n, -1, np.int64)
+                    so = mo = 0
+                    for r, (st, me) in keep:
+                        sptr[r], mptr[r] = so, mo
+                        so += st.shape[0]
+                        mo += me.size
+                    stream = np.concatenate([st for _, (st, _) in keep]).astype(np.int32)
+                    meta = np.concatenate([me for _, (_, me) in keep]).astype(np.int32)
+                    rows = t.from_numpy(np.array([r for r, _ in keep], np.int64)).cuda()
+                    flags_d[rows] = 4
+                    plans = (t.from_numpy(stream.reshape(-1)).cuda(), t.from_numpy(sptr).cuda(),
+                             t.from_numpy(meta).cuda(), t.from_numpy(mptr).cuda(), len(keep))
+        self._hub = (el, plans)
+        return plans
+
     def fwd_schedule(self):
         if self._fwd is None:
             self._fwd, _ = schedule_dev(self.pattern, False, self._classes("fwd"))
@@ -525,6 +580,7 @@ class DevIlu:
             return
         sched = self.factor_schedule()
         el = self.elim_lists()
+        hub = self.hub_plans()
         if lo > 0 or hi < self.n:
             sched = sched.restrict(lo, hi)
         if norms:
@@ -536,7 +592,8 @@ class DevIlu:
                   self.fbox.next_epoch(), ptr(self.err), ptr(self.ticket),
                   ptr(el[0]) if el else None, ptr(el[1]) if el else None,
                   ptr(el[2]) if el else None,
-                  ptr(sched.batch_class()) if sched.nbatch else None, stream())
+                  ptr(sched.batch_class()) if sched.nbatch else None,
+                  *([ptr(x) for x in hub[:4]] if hub else [None] * 4), stream())
 
     def factor(self, lo=0, hi=None, ready_below=0):
         """Factor and return the smallest zero-pivot row (or -1)."""
