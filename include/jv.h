@@ -68,6 +68,9 @@ int jv_set_backoff(unsigned cap_ns);
  * min 16). */
 int jv_set_gate(unsigned mask);
 int jv_set_poll(unsigned cap_ns);
+/* lanes of a factor thread batch that wait and finish together (power of
+ * 2, <= 32; default 32) */
+int jv_set_sfp_group(unsigned g);
 /* diagnostics: record 4 globaltimer stamps per factor batch into buf
  * (device, 16*batches uint64; NULL disables) */
 int jv_set_trace(unsigned long long* buf, long long batches);

@@ -141,6 +141,13 @@ extern "C" int jv_set_poll(unsigned cap_ns) {
   return JV_OK;
 }
 
+extern "C" int jv_set_sfp_group(unsigned g) {
+  if (g == 0 || g > 32 || (g & (g - 1))) { jvh::set_error("jv_set_sfp_group: power of 2 <= 32"); return JV_EINVAL; }
+  cudaError_t e = cudaMemcpyToSymbol(jv::g_sfp_group, &g, sizeof(unsigned));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_sfp_group");
+  return JV_OK;
+}
+
 extern "C" int jv_set_spin_limit(unsigned limit) {
   cudaError_t e = cudaMemcpyToSymbol(jv::g_spin_limit, &limit, sizeof(unsigned));
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_spin_limit");

@@ -1560,6 +1560,7 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
     const int r = active ? A.order[idx] : -1;
     // batch class from the schedule (loaded alongside batch_ptr)
     const int bcls = A.bclass != nullptr ? A.bclass[b] : -1;
+    SfpRow F;
     if (lane == 0) jv::trace_mark(T, b, 1);
     // row flags (jv_elim_lists): 0 thread path, 1 pairable listed warp row,
     // 2 heavy, 3 listed warp row
@@ -1574,7 +1575,6 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
       if (lane == 0) jv::trace_mark(T, b, 4);
       continue;
     }
-    SfpRow F;
     ShortRow R;
     bool sfp = false, fits = false;
     if (active && flag == 0) {
@@ -1595,7 +1595,13 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorArgs A) {
     __syncwarp();
     if (lane == 0) jv::trace_mark(T, b, 3);
     const unsigned smask = __ballot_sync(full, sfp);
-    if (sfp) sfp_finish(A, r, F, smask, b, T);
+    if (sfp) {
+      // lanes complete in groups of g_sfp_group (32: the whole warp waits
+      // for its slowest row; smaller groups finish independently)
+      const unsigned gs = jv::g_sfp_group;
+      const unsigned gmask = gs >= 32 ? 0xffffffffu : (((1u << gs) - 1) << (lane & ~(gs - 1)));
+      sfp_finish(A, r, F, smask & gmask, b, T);
+    }
     const unsigned fmask = __ballot_sync(full, fits);
     if (fits) short_finish(A, r, R, S, fmask, b, T);
     unsigned pend = __ballot_sync(full, active && !fits && !sfp);

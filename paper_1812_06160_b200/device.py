@@ -395,13 +395,14 @@ class DevIlu:
                 cls3 = cls * 2
             self._fsched, self._fwd_levels = schedule_dev(self.pattern, False,
                                                           cls3.to(t.int32).contiguous(),
-                                                          steps=(32, 2, 1),
+                                                          steps=(self.THREAD_BATCH, 2, 1),
                                                           level_of=self._fwd_levels)
             self._fsched_milu = self.milu
         return self._fsched
 
     # heavy rows: structural matches precomputed once per pattern (jv_elim_lists)
     ELIM_MIN_CAND = 256
+    THREAD_BATCH = 32         # thread-path rows per factor batch (24/16/8 measured no better)
     ELIM_WARP_ROWS = True     # lists for every warp-path row, not only heavy ones
 
     def elim_lists(self):

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--rmat-seed", type=int, default=-1)
     ap.add_argument("--gate", type=int, default=None)
     ap.add_argument("--poll", type=int, default=None)
+    ap.add_argument("--group", type=int, default=None)
     args = ap.parse_args()
     import torch
     import paper_1812_06160_b200 as jv
@@ -39,6 +40,8 @@ def main():
         _lib.call("jv_set_gate", args.gate)
     if args.poll is not None:
         _lib.call("jv_set_poll", args.poll)
+    if args.group is not None:
+        _lib.call("jv_set_sfp_group", args.group)
     t0 = time.time()
     if args.rmat_seed >= 0:
         a, base, s = W.rmat(18, args.rmat_seed), None, W.CONFIGS["c5"]
