@@ -71,6 +71,9 @@ int jv_set_poll(unsigned cap_ns);
 /* lanes of a factor thread batch that wait and finish together (power of
  * 2, <= 32; default 32) */
 int jv_set_sfp_group(unsigned g);
+/* solve thread path: dependencies staged by cp.async in two round trips (1)
+ * or probed in register rounds of 12 (0, default: measured faster) */
+int jv_set_solve_staged(unsigned on);
 /* diagnostics: record 4 globaltimer stamps per factor batch into buf
  * (device, 16*batches uint64; NULL disables) */
 int jv_set_trace(unsigned long long* buf, long long batches);

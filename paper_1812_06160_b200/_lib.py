@@ -34,6 +34,7 @@ _SIGS = {
     "jv_set_gate": [ctypes.c_uint],
     "jv_set_poll": [ctypes.c_uint],
     "jv_set_sfp_group": [ctypes.c_uint],
+    "jv_set_solve_staged": [ctypes.c_uint],
     "jv_set_trace": [_P, ctypes.c_longlong],
     "jv_test_ddiv": [c_int32, _P, _P, _P, _P],
     "jv_spmv_tile": [],

@@ -148,6 +148,12 @@ extern "C" int jv_set_sfp_group(unsigned g) {
   return JV_OK;
 }
 
+extern "C" int jv_set_solve_staged(unsigned on) {
+  cudaError_t e = cudaMemcpyToSymbol(jv::g_solve_staged, &on, sizeof(unsigned));
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_solve_staged");
+  return JV_OK;
+}
+
 extern "C" int jv_set_spin_limit(unsigned limit) {
   cudaError_t e = cudaMemcpyToSymbol(jv::g_spin_limit, &limit, sizeof(unsigned));
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_set_spin_limit");

@@ -23,7 +23,11 @@
 
 namespace {
 
-constexpr int kThreadDeps = 32;   // longer rows take the warp path
+constexpr int kThreadDeps = 24;   // staging capacity; thread-path limit per direction below
+// longer rows take the warp path: forward 24, backward 16 dependencies (swept
+// 12-32 on configs 2-4: c4 forward prefers 24, c3/c4 backward 16)
+constexpr int kThreadDepsFwd = 24;
+constexpr int kThreadDepsBwd = 16;
 constexpr int kProbe = 12;        // dependency values probed together per round (swept 8-16)
 constexpr int kWarpBlock = 128;   // warp path: dependencies per prefetched block
 
@@ -94,6 +98,58 @@ JV_INLINE double fold_deps(const SolveArgs& A, int p0, int p1, double s, unsigne
   return s;
 }
 
+// thread path, staged: every dependency of the row (<= kThreadDeps) in two
+// memory round trips — the column indices, then the values and the mailbox
+// packets copied by cp.async into the warp's shared staging area (no
+// registers held per dependency) — then the chain folded from shared
+// memory in the reference order.  Stale packets are re-probed converged.
+struct SolveStage {
+  uint64_t* pk;   // [kThreadDeps][32] packets (2 words)
+  double* v;      // [kThreadDeps][32] values
+  int* c;         // [kThreadDeps][32] columns
+};
+constexpr size_t kSolveStageBytes = (size_t)kThreadDeps * 32 * (16 + 8 + 4);
+
+JV_INLINE double fold_deps_staged(const SolveArgs& A, int p0, int p1, double s, unsigned mask,
+                                  int lane, const SolveStage& St) {
+  const int m = p1 - p0;
+  for (int t = 0; t < m; ++t) {
+    cp_async4(St.c + t * 32 + lane, A.col + p0 + t);
+    cp_async8(St.v + t * 32 + lane, A.val + p0 + t);
+  }
+  cp_commit();
+  cp_wait<0>();
+  for (int t = 0; t < m; ++t)
+    cp_async16(St.pk + 2 * (t * 32 + lane), A.mbox + 2 * (long long)St.c[t * 32 + lane]);
+  cp_commit();
+  cp_wait<0>();
+  // stale packets: converged re-probes, one dependency slot at a time
+  unsigned miss = 0;
+  for (int t = 0; t < m; ++t) {
+    const ulonglong2 pk = *reinterpret_cast<const ulonglong2*>(St.pk + 2 * (t * 32 + lane));
+    if ((uint32_t)(pk.x >> 32) != A.epoch || (uint32_t)(pk.y >> 32) != A.epoch) miss |= 1u << t;
+  }
+  while (__any_sync(mask, miss != 0)) {
+    const int t = miss ? __ffs(miss) - 1 : 0;
+    int cc[1] = {St.c[t * 32 + lane]};
+    double xv[1] = {0.0};
+    gather_conv<1>(A, cc, xv, miss ? 1u : 0u, mask);
+    if (miss) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(xv[0]);
+      const unsigned long long tag = (unsigned long long)A.epoch << 32;
+      St.pk[2 * (t * 32 + lane)] = tag | (b & 0xffffffffull);
+      St.pk[2 * (t * 32 + lane) + 1] = tag | (b >> 32);
+      miss &= miss - 1;
+    }
+  }
+  for (int t = 0; t < m; ++t) {
+    const ulonglong2 pk = *reinterpret_cast<const ulonglong2*>(St.pk + 2 * (t * 32 + lane));
+    const double x = __longlong_as_double((long long)((pk.x & 0xffffffffull) | (pk.y << 32)));
+    s = jv::dsub(s, jv::dmul(St.v[t * 32 + lane], x));
+  }
+  return s;
+}
+
 // warp path: same chain in blocks of 128 dependencies: the probes of block
 // k+1 are issued before block k is folded (one L2 round trip hides behind
 // the fold), products go to shared memory and one lane keeps the
@@ -158,6 +214,13 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
   const int lane = threadIdx.x & 31;
   __shared__ double warp_prod[8][2 * kWarpBlock];
   double* sp = warp_prod[threadIdx.x >> 5];
+  extern __shared__ __align__(16) unsigned char solve_stage[];
+  SolveStage St;
+  St.pk = reinterpret_cast<uint64_t*>(solve_stage + (threadIdx.x >> 5) * kSolveStageBytes);
+  St.v = reinterpret_cast<double*>(solve_stage + (threadIdx.x >> 5) * kSolveStageBytes +
+                                   (size_t)kThreadDeps * 32 * 16);
+  St.c = reinterpret_cast<int*>(solve_stage + (threadIdx.x >> 5) * kSolveStageBytes +
+                                (size_t)kThreadDeps * 32 * 24);
   const int W = (gridDim.x * blockDim.x) >> 5;
   const jv::Trace T = jv::trace_begin();
   for (;;) {
@@ -188,10 +251,11 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
       if (lane == 0 && g >= 0 && (jv::g_gate & 2)) jv::mbox_gate(A.mbox, g, A.epoch);
     }
     __syncwarp();
-    const bool small = p1 - p0 <= kThreadDeps;
+    const bool small = p1 - p0 <= (kBackward ? kThreadDepsBwd : kThreadDepsFwd);
     const unsigned smask = __ballot_sync(full, active && small);
     if (active && small) {
-      double s = fold_deps(A, p0, p1, A.in[r], smask);
+      double s = jv::g_solve_staged ? fold_deps_staged(A, p0, p1, A.in[r], smask, lane, St)
+                                    : fold_deps(A, p0, p1, A.in[r], smask);
       if (kBackward) {
         const double d = __ldg(A.val + dp);
         bool slow;
@@ -228,7 +292,7 @@ __global__ void classify_solve_kernel(int n, const int32_t* rs, const int32_t* d
                                       int32_t* cls) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int deps = backward ? rs[r + 1] - diag[r] - 1 : diag[r] - rs[r];
-    cls[r] = deps > kThreadDeps ? 1 : 0;
+    cls[r] = deps > (backward ? kThreadDepsBwd : kThreadDepsFwd) ? 1 : 0;
   }
 }
 
@@ -247,8 +311,10 @@ extern "C" int jv_solve(int which, int32_t n, const int32_t* row_start, const in
   SolveArgs A{row_start, col, val, diag_pos, order, batch_ptr, nbatch, in, out, mbox, epoch, ticket};
   void* args[] = {&A};
   if (which == 0)
-    return jvh::persistent_launch(solve_kernel<false>, 256, args, (cudaStream_t)stream, "jv_solve fwd");
-  return jvh::persistent_launch(solve_kernel<true>, 256, args, (cudaStream_t)stream, "jv_solve bwd");
+    return jvh::persistent_launch(solve_kernel<false>, 256, args, (cudaStream_t)stream, "jv_solve fwd",
+                                  8 * kSolveStageBytes);
+  return jvh::persistent_launch(solve_kernel<true>, 256, args, (cudaStream_t)stream, "jv_solve bwd",
+                                8 * kSolveStageBytes);
 }
 
 extern "C" int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,

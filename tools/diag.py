@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--gate", type=int, default=None)
     ap.add_argument("--poll", type=int, default=None)
     ap.add_argument("--group", type=int, default=None)
+    ap.add_argument("--staged", type=int, default=None)
     args = ap.parse_args()
     import torch
     import paper_1812_06160_b200 as jv
@@ -42,6 +43,8 @@ def main():
         _lib.call("jv_set_poll", args.poll)
     if args.group is not None:
         _lib.call("jv_set_sfp_group", args.group)
+    if args.staged is not None:
+        _lib.call("jv_set_solve_staged", args.staged)
     t0 = time.time()
     if args.rmat_seed >= 0:
         a, base, s = W.rmat(18, args.rmat_seed), None, W.CONFIGS["c5"]
