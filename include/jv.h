@@ -106,6 +106,23 @@ int jv_gather(int32_t n, const int32_t* idx, const double* src, double* dst, voi
  * every entry point below serves them unchanged and the level schedule of
  * the block-diagonal matrix interleaves all blocks automatically. */
 
+/* ---- vector kernels of the device Krylov driver (krylov.py) -----------
+ * replace the numpy vector ops of krylov.py:52-151 (pcg / gmres).  Dot
+ * products are deterministic (fixed grid of partial sums, summed in order);
+ * ws = device workspace of jv_dot_workspace() doubles; out / rr device
+ * scalars.  Updates are explicitly rounded (no FMA), as numpy's.        */
+int jv_dot_workspace(void);
+int jv_dot(int64_t n, const double* x, const double* y, double* ws, double* out, int sqrt_out,
+           void* stream);
+/* y += a*x, with a = sign * (*coef_dev) when coef_dev is not NULL */
+int jv_axpy(int64_t n, double a, const double* coef_dev, double sign, const double* x, double* y,
+            void* stream);
+int jv_xpby(int64_t n, const double* x, double b, double* y, void* stream);   /* y = x + b y */
+int jv_scale(int64_t n, double a, const double* x, double* y, void* stream);  /* y = a x */
+/* PCG step (krylov.py:72-79): x += alpha p ; r -= alpha ap ; *rr = r.r */
+int jv_pcg_update(int64_t n, double alpha, const double* p, const double* ap, double* x,
+                  double* r, double* ws, double* rr, void* stream);
+
 /* ---- setup (bit-exact structure) ------------------------------------- */
 /* Longest-path depth over the columns < r of each row (forward,
  * _kernels.py:37-48, whose input is already strictly lower) or the columns

@@ -64,6 +64,12 @@ _SIGS = {
     "jv_build_schedule": [c_int32, _P, _P, c_int32, _P, _P, _I32P, _P],
     "jv_hub_plan_host": [c_int32, c_int32, _P, _P, _P, _P, _P, POINTER(c_int64), _P,
                          POINTER(c_int64)],
+    "jv_dot_workspace": [],
+    "jv_dot": [c_int64, _P, _P, _P, _P, c_int, _P],
+    "jv_axpy": [c_int64, c_double, _P, c_double, _P, _P, _P],
+    "jv_xpby": [c_int64, _P, c_double, _P, _P],
+    "jv_scale": [c_int64, c_double, _P, _P, _P],
+    "jv_pcg_update": [c_int64, c_double, _P, _P, _P, _P, _P, _P, _P],
     "jv_build_schedule_n": [c_int32, _P, _P, c_int32, c_int32, _P, _P, _P, _I32P, _P],
     "jv_classify_factor": [c_int32, _P, _P, _P, c_int, _P, _P],
     "jv_classify_solve": [c_int, c_int32, _P, _P, _P, _P],

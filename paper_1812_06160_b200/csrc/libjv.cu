@@ -7,4 +7,5 @@
 #include "setup.cu"
 #include "elim.cu"
 #include "region.cu"
+#include "blas.cu"
 #include "host.cpp"
