@@ -289,29 +289,39 @@ int jv_classify_factor(int32_t n, const int32_t* row_start, const int32_t* col,
 int jv_classify_solve(int which, int32_t n, const int32_t* row_start, const int32_t* diag_pos,
                       int32_t* cls, void* stream);
 
-/* ---- CTA-resident region factorization (stencil-class matrices) ------
- * Setup (host C++): BFS-grown regions over the symmetrized pattern, rows
- * ordered by level inside each region and cut into waves of
- * jv_region_threads() rows (sign bit of wave_beg = level ends here);
- * per-slot descriptors (returns the count of rows that are NOT
- * stencil-class: the region kernel needs 0).  See csrc/region.cu. */
-int64_t jv_region_plan_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h,
-                            const int32_t* level_h, int32_t nreg, int32_t wave,
-                            int32_t* region_of_h, int32_t* slot_row_h, int32_t* slot_of_h,
-                            int32_t* reg_ptr_h, int32_t* wave_ptr_h, int32_t* wave_beg_h);
-int64_t jv_region_desc_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h,
-                            const int32_t* diag_h, const int32_t* region_of_h,
-                            const int32_t* slot_row_h, const int32_t* slot_of_h,
-                            const int32_t* reg_ptr_h, int32_t* info_h, int32_t* drs_h,
-                            int32_t* ref_h, int32_t* us_h);
+/* ---- CTA-resident region kernels (csrc/region.cu, regions_host.cpp) ---
+ * One co-resident CTA per region of an acyclic box-like partition of the
+ * lower DAG; in-region dependencies through shared memory, cross-region
+ * ones through the 16-byte mailboxes.  Same results as the ticket kernels
+ * (bitwise).  Setup on the host:
+ *   jv_region_partition_host  region id per row (returns #regions or -1);
+ *   jv_rstream_build          wave stream of one direction (kind 0 factor of
+ *                             a stencil-class matrix, 1 forward, 2 backward);
+ *                             sizes[10] = {static bytes, waves, nreg,
+ *                             max_region, max_waves, S, D, CS, CD, remote
+ *                             deps}; returns a handle > 0, -1 (a row does not
+ *                             qualify) or -2 (shared memory too small);
+ *   jv_rstream_export         copies the stream out and frees the handle.
+ * jv_region_run replaces factor_serial_kernel (_kernels.py:197-204) for
+ * kind 0 and the solve kernels (_kernels.py:348-366) for kinds 1/2. */
+int32_t jv_region_partition_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h,
+                                 const int32_t* diag_h, int32_t nreg_max, int32_t max_rows,
+                                 int32_t* region_of_h);
+int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* row_start_h,
+                         const int32_t* col_h, const int32_t* diag_h, const int32_t* region_of_h,
+                         int32_t nreg, int32_t threads, int64_t smem_budget, int32_t tau_norms,
+                         int64_t* sizes_h);
+int jv_rstream_export(int64_t handle, int32_t* words_h, int32_t* table_h, int32_t* reg_wave_h);
 int jv_region_threads(void);
-/* replaces factor_serial_kernel (_kernels.py:197-204) for stencil-class
- * matrices: one co-resident CTA per region, bitwise equal results */
-int jv_factor_regions(int32_t n, int32_t nreg, const int32_t* slot_row, const int32_t* info,
-                      const int32_t* drs, const int32_t* ref, const int32_t* us,
-                      const int32_t* reg_ptr, const int32_t* wave_ptr, const int32_t* wave_beg,
-                      int32_t max_region, double* val, const double* norms, double tau,
-                      uint64_t* mbox, uint32_t epoch, int32_t* err_row, void* stream);
+/* diagnostic switches of the region kernels (bit 0: proxy fence before each
+ * static bulk copy, bit 1: no late mailbox re-probes) */
+int jv_set_region_flags(unsigned flags);
+int64_t jv_region_smem_fixed(int32_t max_region, int32_t max_waves);
+int jv_region_run(int32_t kind, int32_t nreg, const void* words, const int32_t* table,
+                  const int32_t* reg_wave, int32_t max_region, int32_t max_waves, int32_t S,
+                  int32_t D, int32_t CS, int32_t CD, double* val, const double* in, double* out,
+                  const double* norms, double tau, uint64_t* mbox, uint32_t epoch,
+                  int32_t* err_row, void* stream);
 
 #ifdef __cplusplus
 }

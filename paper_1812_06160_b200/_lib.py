@@ -73,18 +73,22 @@ _SIGS = {
     "jv_build_schedule_n": [c_int32, _P, _P, c_int32, c_int32, _P, _P, _P, _I32P, _P],
     "jv_classify_factor": [c_int32, _P, _P, _P, c_int, _P, _P],
     "jv_classify_solve": [c_int, c_int32, _P, _P, _P, _P],
-    "jv_region_plan_host": [c_int32, _P, _P, _P, c_int32, c_int32, _P, _P, _P, _P, _P, _P],
-    "jv_region_desc_host": [c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
-    "jv_factor_regions": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, _P, _P,
-                          c_double, _P, c_uint32, _P, _P],
+    "jv_region_partition_host": [c_int32, _P, _P, _P, c_int32, c_int32, _P],
+    "jv_rstream_build": [c_int32, c_int32, _P, _P, _P, _P, c_int32, c_int32, c_int64, c_int32, _P],
+    "jv_rstream_export": [c_int64, _P, _P, _P],
+    "jv_region_smem_fixed": [c_int32, c_int32],
+    "jv_region_run": [c_int32, c_int32, _P, _P, _P, c_int32, c_int32, c_int32, c_int32, c_int32,
+                      c_int32, _P, _P, _P, _P, c_double, _P, c_uint32, _P, _P],
     "jv_region_threads": [],
+    "jv_set_region_flags": [ctypes.c_uint],
 }
 _RESTYPES = {
     "jv_last_error": ctypes.c_char_p,
     "jv_iluk_host": c_int64,
     "jv_free_host": None,
-    "jv_region_plan_host": c_int64,
-    "jv_region_desc_host": c_int64,
+    "jv_region_partition_host": c_int32,
+    "jv_rstream_build": c_int64,
+    "jv_region_smem_fixed": c_int64,
 }
 
 _lib = None

@@ -176,174 +176,6 @@ extern "C" int64_t jv_iluk_host(int32_t n, const int32_t* rs, const int32_t* col
 extern "C" void jv_free_host(void* p) { free(p); }
 
 // ---------------------------------------------------------------------------
-// Region plan for the CTA-resident factorization / solves (setup, host C++).
-//
-// Rows are split into `nreg` regions grown by BFS over the symmetrized
-// factor pattern (each region = one CTA; compact regions keep most
-// dependency hops inside an SM).  Inside a region rows are ordered by level
-// (levels of the sweep's DAG, given), then split into waves of <= `wave`
-// rows; a wave that ends a level carries the SYNC flag (the CTA barrier).
-// Outputs (caller-allocated, host):
-//   region_of[n]                region id per row
-//   slot_row[n]                 rows in (region, level, row) order
-//   slot_of[n]                  inverse of slot_row
-//   reg_ptr[nreg+1]             slot range per region
-//   wave_ptr[nreg+1]            wave range per region (into wave_beg)
-//   wave_beg[n + nlevels*nreg]  first slot of each wave, |= 1<<31 when the wave
-//                               ends a level (barrier after it); terminated
-//                               by reg_ptr (the next wave's start)
-// Returns the number of waves or < 0.
-extern "C" int64_t jv_region_plan_host(int32_t n, const int32_t* rs, const int32_t* col,
-                                       const int32_t* level, int32_t nreg, int32_t wave,
-                                       int32_t* region_of, int32_t* slot_row, int32_t* slot_of,
-                                       int32_t* reg_ptr, int32_t* wave_ptr, int32_t* wave_beg) {
-  if (n < 0 || nreg < 1 || wave < 1) return JV_EINVAL;
-  // symmetrized adjacency (pattern may be unsymmetric)
-  std::vector<int64_t> deg(n + 1, 0);
-  for (int32_t i = 0; i < n; ++i)
-    for (int32_t p = rs[i]; p < rs[i + 1]; ++p) {
-      const int32_t j = col[p];
-      if (j == i) continue;
-      ++deg[i];
-      ++deg[j];
-    }
-  std::vector<int64_t> aptr(n + 1, 0);
-  for (int32_t i = 0; i < n; ++i) aptr[i + 1] = aptr[i] + deg[i];
-  std::vector<int32_t> adj(aptr[n]);
-  std::vector<int64_t> fill(aptr.begin(), aptr.end() - 1);
-  for (int32_t i = 0; i < n; ++i)
-    for (int32_t p = rs[i]; p < rs[i + 1]; ++p) {
-      const int32_t j = col[p];
-      if (j == i) continue;
-      adj[fill[i]++] = j;
-      adj[fill[j]++] = i;
-    }
-  const int64_t target = (n + nreg - 1) / nreg;
-  // a caller-supplied partition (region_of[0] >= 0 on entry) is kept as is
-  const bool given = n > 0 && region_of[0] >= 0;
-  if (!given)
-    for (int32_t i = 0; i < n; ++i) region_of[i] = -1;
-  std::vector<int32_t> queue;
-  queue.reserve(n);
-  int32_t seed = 0;
-  int32_t g = 0;
-  int64_t count = 0;
-  size_t head = 0;
-  queue.clear();
-  while (!given) {
-    if (head == queue.size()) {
-      // start (or continue) BFS from the lowest unassigned row
-      while (seed < n && region_of[seed] >= 0) ++seed;
-      if (seed == n) break;
-      region_of[seed] = g;
-      queue.push_back(seed);
-      if (++count == target && g < nreg - 1) { ++g; count = 0; queue.clear(); head = 0; }
-      continue;
-    }
-    const int32_t v = queue[head++];
-    for (int64_t p = aptr[v]; p < aptr[v + 1]; ++p) {
-      const int32_t w = adj[p];
-      if (region_of[w] >= 0) continue;
-      region_of[w] = g;
-      queue.push_back(w);
-      if (++count == target && g < nreg - 1) {
-        ++g;
-        count = 0;
-        queue.clear();
-        head = 0;
-        break;
-      }
-    }
-  }
-  // slots: sort rows by (region, level, index)
-  std::vector<int32_t> order(n);
-  for (int32_t i = 0; i < n; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-    if (region_of[a] != region_of[b]) return region_of[a] < region_of[b];
-    return level[a] < level[b];
-  });
-  for (int32_t i = 0; i < n; ++i) {
-    slot_row[i] = order[i];
-    slot_of[order[i]] = i;
-  }
-  for (int32_t r = 0; r <= nreg; ++r) reg_ptr[r] = 0;
-  for (int32_t i = 0; i < n; ++i) ++reg_ptr[region_of[i] + 1];
-  for (int32_t r = 0; r < nreg; ++r) reg_ptr[r + 1] += reg_ptr[r];
-  int64_t nw = 0;
-  for (int32_t r = 0; r < nreg; ++r) {
-    wave_ptr[r] = (int32_t)nw;
-    int32_t i = reg_ptr[r];
-    while (i < reg_ptr[r + 1]) {
-      const int32_t lev = level[slot_row[i]];
-      int32_t e = i;
-      while (e < reg_ptr[r + 1] && level[slot_row[e]] == lev) ++e;
-      for (int32_t s = i; s < e; s += wave) {
-        const bool last = s + wave >= e;
-        wave_beg[nw++] = s | (last ? (int32_t)0x80000000u : 0);
-      }
-      i = e;
-    }
-  }
-  wave_ptr[nreg] = (int32_t)nw;
-  return nw;
-}
-
-// Per-slot descriptors of the stencil region factorization (setup, host).
-// A row qualifies when it has <= 4 pivots and every pivot's U row meets it
-// only at its diagonal (see factor.cu, stencil fast path).  For slot i:
-//   info[i] = nL | pub << 3 | (u-mask) << 4     pub: a row of another region
-//                                                reads this row's diagonal
-//   drs[i]  = row_start of the slot's row
-//   ref[k*n + i] >= 0: pivot k's slot inside the region; < 0: -(1 + diag
-//                position of pivot k) — a remote pivot, read from the mailbox
-//   us[k*n + i]  = position of u(c_k, r) in val (valid when u-mask bit k)
-// Returns the number of rows that do not qualify (0: the region kernel
-// applies to the whole matrix).
-extern "C" int64_t jv_region_desc_host(int32_t n, const int32_t* rs, const int32_t* col,
-                                       const int32_t* diag, const int32_t* region_of,
-                                       const int32_t* slot_row, const int32_t* slot_of,
-                                       const int32_t* reg_ptr, int32_t* info, int32_t* drs,
-                                       int32_t* ref, int32_t* us) {
-  std::vector<int32_t> mark(n, -1);
-  std::vector<char> pub(n, 0);
-  int64_t bad = 0;
-  for (int32_t r = 0; r < n; ++r) {
-    const int32_t nL = diag[r] - rs[r];
-    for (int32_t k = 0; k < nL; ++k) {
-      const int32_t c = col[rs[r] + k];
-      if (region_of[c] != region_of[r]) pub[c] = 1;
-    }
-  }
-  for (int32_t i = 0; i < n; ++i) {
-    const int32_t r = slot_row[i];
-    const int32_t g = region_of[r];
-    const int32_t nL = diag[r] - rs[r];
-    drs[i] = rs[r];
-    for (int32_t k = 0; k < 4; ++k) {
-      ref[(int64_t)k * n + i] = 0;
-      us[(int64_t)k * n + i] = 0;
-    }
-    if (nL > 4) { ++bad; info[i] = 7; continue; }
-    for (int32_t p = rs[r]; p < rs[r + 1]; ++p) mark[col[p]] = r;
-    int32_t umask = 0;
-    bool ok = true;
-    for (int32_t k = 0; k < nL; ++k) {
-      const int32_t c = col[rs[r] + k];
-      const int32_t dq = diag[c];
-      for (int32_t q = dq + 1; q < rs[c + 1]; ++q) {
-        const int32_t j = col[q];
-        if (j == r) { us[(int64_t)k * n + i] = q; umask |= 1 << k; }
-        else if (mark[j] == r) ok = false;
-      }
-      ref[(int64_t)k * n + i] = region_of[c] == g ? slot_of[c] - reg_ptr[g] : -(dq + 1);
-    }
-    if (!ok) ++bad;
-    info[i] = nL | (pub[r] ? 8 : 0) | (umask << 4);
-  }
-  return bad;
-}
-
-// ---------------------------------------------------------------------------
 // Hub-row gather plan (setup, host): the target-parallel schedule of one
 // heavy row's elimination, so the numeric kernel folds many positions at
 // once instead of walking the pivots one by one.

@@ -7,5 +7,6 @@
 #include "setup.cu"
 #include "elim.cu"
 #include "region.cu"
+#include "regions_host.cpp"
 #include "blas.cu"
 #include "host.cpp"

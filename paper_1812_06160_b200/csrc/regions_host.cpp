@@ -1,0 +1,504 @@
+// Region plans (setup, host C++) for the CTA-resident region kernels
+// (region.cu): one co-resident CTA per region walks its rows level by level,
+// in-region dependencies through shared memory, cross-region ones through
+// the 16-byte mailboxes.
+//
+// 1. Partition (jv_region_partition_host).  A region pipeline is only fast
+//    when the quotient graph of the regions is ACYCLIC: then every region
+//    lags its upstream neighbours by one mailbox hop and runs its levels at
+//    CTA-barrier speed, instead of paying a hop per level.  Any topological
+//    order tau of the DAG gives an acyclic partition by contiguous ranges;
+//    lexicographic refinement by further topological orders keeps it acyclic
+//    (cells (a, b, c) in lexicographic order are a topological order of the
+//    cells).  The orders come from depth-first Kahn sorts (LIFO ready stack)
+//    whose successor lists are rotated by t = 0, 1, 2: on a stencil DAG each
+//    rotation sweeps a different grid axis slowest (measured on config 2:
+//    |corr(position, axis)| = 1.0 for one axis each), so the cells come out
+//    as boxes — a domain decomposition found from the pattern alone.
+// 2. Wave streams (jv_rstream_build / _export).  Per direction (factor,
+//    forward, backward): rows of each region in (level, row) order = local
+//    slots; consecutive rows of one level in waves of <= threads rows; every
+//    wave is a 16-byte aligned structure-of-arrays block of int32 words
+//        [cnt, slot0, K, NP, row[cnt], p0[cnt], meta[cnt], ref[K][cnt],
+//         (factor) us[K][cnt], pslot[NP]]
+//    K = most dependencies of a row in the wave, meta = ndep | pub << 6 |
+//    umask << 7 (factor), ref >= 0: slot in the region's ring, < 0:
+//    -(1 + j), the wave's j-th remote dependency, mailbox slot pslot[j];
+//    us = positions of u(c_k, r) (factor).  The wave's dynamic block holds
+//    vals[NV][cnt] (matrix values, right-hand side; gathered at run time)
+//    and NP 16-byte mailbox packets.  Static blocks are bulk-copied (TMA) S waves ahead into
+//    a shared-memory ring, dynamic blocks gathered D waves ahead; ring
+//    offsets are placed here by simulating both FIFO rings.
+#include "../../include/jv.h"
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+namespace {
+
+// successor lists of the lower DAG (edge c -> r for every strictly-lower
+// entry (r, c)), each list ascending
+void lower_successors(int32_t n, const int32_t* rs, const int32_t* col, const int32_t* diag,
+                      std::vector<int64_t>& sptr, std::vector<int32_t>& succ,
+                      std::vector<int32_t>& indeg) {
+  sptr.assign(n + 1, 0);
+  indeg.assign(n, 0);
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t p = rs[r]; p < diag[r]; ++p) {
+      ++sptr[col[p] + 1];
+      ++indeg[r];
+    }
+  for (int32_t i = 0; i < n; ++i) sptr[i + 1] += sptr[i];
+  succ.resize(sptr[n]);
+  std::vector<int64_t> fill(sptr.begin(), sptr.end() - 1);
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t p = rs[r]; p < diag[r]; ++p) succ[fill[col[p]]++] = r;
+}
+
+// depth-first Kahn order, successor lists rotated by t; pos[v] = position
+void lifo_order(int32_t n, const std::vector<int64_t>& sptr, const std::vector<int32_t>& succ,
+                std::vector<int32_t> indeg, int t, std::vector<int32_t>& pos) {
+  std::vector<int32_t> stack;
+  stack.reserve(n);
+  for (int32_t v = n - 1; v >= 0; --v)
+    if (indeg[v] == 0) stack.push_back(v);
+  pos.assign(n, -1);
+  int32_t k = 0;
+  while (!stack.empty()) {
+    const int32_t v = stack.back();
+    stack.pop_back();
+    pos[v] = k++;
+    const int64_t a = sptr[v], len = sptr[v + 1] - a;
+    if (len == 0) continue;
+    const int64_t rot = t % len;
+    for (int64_t i = 0; i < len; ++i) {
+      const int32_t w = succ[a + (i + rot) % len];
+      if (--indeg[w] == 0) stack.push_back(w);
+    }
+  }
+}
+
+}  // namespace
+
+// Acyclic region partition of the lower DAG of a combined L|U pattern.
+// nreg_max regions at most (one CTA per SM), each <= max_rows rows.
+// region_of[r] receives the region id; returns the number of regions, or
+// -1 when the rows do not fit (n > nreg * max_rows).
+extern "C" int32_t jv_region_partition_host(int32_t n, const int32_t* rs, const int32_t* col,
+                                            const int32_t* diag, int32_t nreg_max,
+                                            int32_t max_rows, int32_t* region_of) {
+  if (n <= 0 || nreg_max < 1) return -1;
+  std::vector<int64_t> sptr;
+  std::vector<int32_t> succ, indeg;
+  lower_successors(n, rs, col, diag, sptr, succ, indeg);
+  int64_t maxs = 0;
+  for (int32_t v = 0; v < n; ++v) maxs = std::max(maxs, sptr[v + 1] - sptr[v]);
+  const int dims = (int)std::max<int64_t>(1, std::min<int64_t>(3, maxs));
+  // balanced factorisation of <= nreg_max parts into `dims` factors
+  int best[3] = {nreg_max, 1, 1};
+  int64_t bprod = dims == 1 ? nreg_max : 0;
+  double bratio = 1e30;
+  if (dims > 1) {
+    for (int a = 1; a <= nreg_max; ++a)
+      for (int b = 1; b <= a && (int64_t)a * b <= nreg_max; ++b) {
+        int c = 1;
+        if (dims == 3) {
+          c = nreg_max / (a * b);
+          c = std::min(c, b);
+          if (c < 1) continue;
+        }
+        const int64_t prod = (int64_t)a * b * c;
+        const double ratio = (double)a / (dims == 3 ? c : b);
+        if (ratio > 1.6) continue;
+        if (prod > bprod || (prod == bprod && ratio < bratio)) {
+          bprod = prod;
+          bratio = ratio;
+          best[0] = a;
+          best[1] = b;
+          best[2] = dims == 3 ? c : 1;
+        }
+      }
+  }
+  int64_t nparts = (int64_t)best[0] * best[1] * best[2];
+  while (nparts > 1 && (int64_t)n < nparts) {   // tiny matrices: fewer regions
+    for (int d = 0; d < 3; ++d)
+      if (best[d] > 1) { --best[d]; break; }
+    nparts = (int64_t)best[0] * best[1] * best[2];
+  }
+  if ((n + nparts - 1) / nparts > max_rows) return -1;
+  std::vector<int32_t> reg(n, 0), pos, idx(n), next(n);
+  int32_t ngroups = 1;
+  for (int d = 0; d < dims; ++d) {
+    const int p = best[d];
+    lifo_order(n, sptr, succ, indeg, d, pos);
+    for (int32_t i = 0; i < n; ++i) idx[i] = i;
+    std::sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+      return reg[a] != reg[b] ? reg[a] < reg[b] : pos[a] < pos[b];
+    });
+    int32_t i = 0;
+    while (i < n) {
+      int32_t e = i;
+      const int32_t g = reg[idx[i]];
+      while (e < n && reg[idx[e]] == g) ++e;
+      const int64_t cnt = e - i;
+      for (int32_t k = i; k < e; ++k) next[idx[k]] = g * p + (int32_t)(((int64_t)(k - i) * p) / cnt);
+      i = e;
+    }
+    reg.swap(next);
+    ngroups *= p;
+  }
+  // compact ids (empty cells are possible only for tiny inputs)
+  std::vector<int32_t> remap(ngroups, -1);
+  int32_t nreg = 0;
+  for (int32_t r = 0; r < n; ++r)
+    if (remap[reg[r]] < 0) remap[reg[r]] = 0;
+  for (int32_t g = 0; g < ngroups; ++g)
+    if (remap[g] == 0) remap[g] = nreg++;
+  for (int32_t r = 0; r < n; ++r) region_of[r] = remap[reg[r]];
+  return nreg;
+}
+
+namespace {
+
+struct RStream {
+  int kind = 0;
+  int32_t nreg = 0, max_region = 0, max_waves = 0;
+  int32_t S = 0, D = 0, CS = 0, CD = 0, SC = 0;
+  std::vector<int32_t> words;     // static stream (16-byte aligned blocks)
+  std::vector<int32_t> table;     // int4 per wave {goff16, bytes, soff, doff}
+  std::vector<int32_t> reg_wave;  // nreg + 1
+  int64_t nrows_remote = 0, ndeps_remote = 0;
+};
+
+std::mutex g_rs_mu;
+std::map<int64_t, std::unique_ptr<RStream>> g_rs;
+int64_t g_rs_next = 1;
+
+// FIFO ring placement: block w may not overlap blocks w-window .. w-1
+bool ring_place(const std::vector<int32_t>& sz, int32_t cap, int window,
+                std::vector<int32_t>& off) {
+  off.assign(sz.size(), 0);
+  int64_t head = 0;
+  for (size_t w = 0; w < sz.size(); ++w) {
+    const int64_t s = sz[w];
+    if (s > cap) return false;
+    int64_t o = head;
+    if (o + s > cap) o = 0;
+    for (size_t v = w > (size_t)window ? w - window : 0; v < w; ++v) {
+      const int64_t a = off[v], b = a + sz[v];
+      if (s > 0 && sz[v] > 0 && o < b && a < o + s) return false;
+    }
+    off[w] = (int32_t)o;
+    head = o + s;
+  }
+  return true;
+}
+
+int32_t min_cap(const std::vector<std::vector<int32_t>>& per_region, int window, int32_t budget) {
+  // smallest capacity (16-byte steps) that places every region's blocks
+  int32_t lo = 16;
+  for (auto& v : per_region)
+    for (int32_t s : v) lo = std::max(lo, s);
+  std::vector<int32_t> off;
+  auto fits = [&](int32_t cap) {
+    for (auto& v : per_region)
+      if (!ring_place(v, cap, window, off)) return false;
+    return true;
+  };
+  if (lo > budget || !fits(budget)) return -1;
+  int32_t hi = budget;   // fits(hi); binary search in 16-byte steps
+  lo = (lo + 15) & ~15;
+  while (lo < hi) {
+    const int32_t mid = ((lo + (hi - lo) / 2) + 15) & ~15;
+    if (mid >= hi) break;
+    if (fits(mid)) hi = mid;
+    else lo = mid + 16;
+  }
+  return fits(lo) ? lo : hi;
+}
+
+}  // namespace
+
+// Build a wave stream.  kind 0: factorization (stencil-class rows only:
+// <= 4 pivots, every pivot's U row meets the row only at its diagonal),
+// 1: forward solve (unit L), 2: backward solve.  threads = rows per wave,
+// smem_budget = shared memory the kernel may use (bytes), tau_norms = the
+// factor gathers each row's norm (tau > 0).  sizes[0..9] receive
+// {static bytes, total waves, nreg, max_region, max_waves, S, D, CS, CD,
+// remote-dependency count}.  Returns a handle > 0, or
+// -1 (a row does not qualify), -2 (does not fit in shared memory).
+extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, const int32_t* col,
+                                    const int32_t* diag, const int32_t* region_of, int32_t nreg,
+                                    int32_t threads, int64_t smem_budget, int32_t tau_norms,
+                                    int64_t* sizes) {
+  if (n <= 0 || nreg < 1 || threads < 32) return -1;
+  auto R = std::make_unique<RStream>();
+  R->kind = kind;
+  R->nreg = nreg;
+  const bool fwd = kind != 2;
+  // dependencies of row r (ascending column): fwd/factor = strict lower,
+  // bwd = strict upper
+  auto dep_lo = [&](int32_t r) { return fwd ? rs[r] : diag[r] + 1; };
+  auto dep_hi = [&](int32_t r) { return fwd ? diag[r] : rs[r + 1]; };
+  // levels of this direction's DAG
+  std::vector<int32_t> lev(n, 0);
+  if (fwd) {
+    for (int32_t r = 0; r < n; ++r) {
+      int32_t l = 0;
+      for (int32_t p = dep_lo(r); p < dep_hi(r); ++p) l = std::max(l, lev[col[p]] + 1);
+      lev[r] = l;
+    }
+  } else {
+    for (int32_t r = n - 1; r >= 0; --r) {
+      int32_t l = 0;
+      for (int32_t p = dep_lo(r); p < dep_hi(r); ++p) l = std::max(l, lev[col[p]] + 1);
+      lev[r] = l;
+    }
+  }
+  // qualification (factor: stencil class) and per-row u positions
+  std::vector<int32_t> us;
+  std::vector<int32_t> umask;
+  if (kind == 0) {
+    us.assign((size_t)4 * n, 0);
+    umask.assign(n, 0);
+    std::vector<int32_t> mark(n, -1);
+    for (int32_t r = 0; r < n; ++r) {
+      const int32_t nL = diag[r] - rs[r];
+      if (nL > 4) return -1;
+      for (int32_t p = rs[r]; p < rs[r + 1]; ++p) mark[col[p]] = r;
+      for (int32_t k = 0; k < nL; ++k) {
+        const int32_t c = col[rs[r] + k];
+        for (int32_t q = diag[c] + 1; q < rs[c + 1]; ++q) {
+          const int32_t j = col[q];
+          if (j == r) {
+            us[(size_t)4 * r + k] = q;
+            umask[r] |= 1 << k;
+          } else if (mark[j] == r) {
+            return -1;   // the pivot's U row meets row r off the diagonal
+          }
+        }
+      }
+    }
+  } else {
+    for (int32_t r = 0; r < n; ++r)
+      if (dep_hi(r) - dep_lo(r) > 32) return -1;
+  }
+  // slots: rows of each region in (level, row) order
+  std::vector<int32_t> reg_ptr(nreg + 1, 0);
+  for (int32_t r = 0; r < n; ++r) {
+    if (region_of[r] < 0 || region_of[r] >= nreg) return -1;
+    ++reg_ptr[region_of[r] + 1];
+  }
+  for (int32_t g = 0; g < nreg; ++g) reg_ptr[g + 1] += reg_ptr[g];
+  std::vector<int32_t> slot_row(n), slot_of(n);
+  {
+    std::vector<int32_t> fill(reg_ptr.begin(), reg_ptr.end() - 1);
+    for (int32_t r = 0; r < n; ++r) slot_row[fill[region_of[r]]++] = r;
+    for (int32_t g = 0; g < nreg; ++g)
+      std::stable_sort(slot_row.begin() + reg_ptr[g], slot_row.begin() + reg_ptr[g + 1],
+                       [&](int32_t a, int32_t b) { return lev[a] < lev[b]; });
+    for (int32_t i = 0; i < n; ++i) slot_of[slot_row[i]] = i;
+  }
+  // waves: consecutive rows of one level, <= threads rows
+  std::vector<int32_t> wave_first, wave_cnt, wave_of_slot(n);
+  R->reg_wave.assign(nreg + 1, 0);
+  for (int32_t g = 0; g < nreg; ++g) {
+    R->max_region = std::max(R->max_region, reg_ptr[g + 1] - reg_ptr[g]);
+    int32_t i = reg_ptr[g];
+    while (i < reg_ptr[g + 1]) {
+      const int32_t l = lev[slot_row[i]];
+      int32_t e = i;
+      while (e < reg_ptr[g + 1] && lev[slot_row[e]] == l && e - i < threads) ++e;
+      for (int32_t k = i; k < e; ++k) wave_of_slot[k] = (int32_t)wave_first.size();
+      wave_first.push_back(i);
+      wave_cnt.push_back(e - i);
+      i = e;
+    }
+    R->reg_wave[g + 1] = (int32_t)wave_first.size();
+    R->max_waves = std::max(R->max_waves, R->reg_wave[g + 1] - R->reg_wave[g]);
+  }
+  const int64_t nw = (int64_t)wave_first.size();
+  // In-region dependency values live in a ring of SC slots (slot i at
+  // i % SC): a dependency is read from it when the slot cannot have been
+  // overwritten — (last slot of the reading wave) - slot(c) < SC — and
+  // through the mailbox otherwise, like a remote one.
+  int64_t need = 1;
+  for (int32_t r = 0; r < n; ++r) {
+    const int32_t wv = wave_of_slot[slot_of[r]];
+    const int32_t last = wave_first[wv] + wave_cnt[wv] - 1;
+    for (int32_t p = dep_lo(r); p < dep_hi(r); ++p)
+      if (region_of[col[p]] == region_of[r]) need = std::max<int64_t>(need, last - slot_of[col[p]] + 1);
+  }
+  int64_t sc_need = 64;
+  while (sc_need < need) sc_need <<= 1;
+  std::vector<char> pub(n, 0);
+  std::vector<int32_t> goff(nw), sbytes(nw), dbytes(nw);
+  std::vector<std::vector<int32_t>> ssz(nreg), dsz(nreg);
+  std::vector<int32_t>& W = R->words;
+  auto local = [&](int32_t r, int32_t c, int32_t SC) {
+    if (region_of[c] != region_of[r]) return false;
+    const int32_t wv = wave_of_slot[slot_of[r]];
+    return wave_first[wv] + wave_cnt[wv] - 1 - slot_of[c] < SC;
+  };
+  auto emit = [&](int32_t SC) {
+    std::fill(pub.begin(), pub.end(), 0);
+    for (int32_t r = 0; r < n; ++r)
+      for (int32_t p = dep_lo(r); p < dep_hi(r); ++p)
+        if (!local(r, col[p], SC)) pub[col[p]] = 1;
+    W.clear();
+    R->ndeps_remote = R->nrows_remote = 0;
+    int32_t g = 0;
+    for (int32_t gg = 0; gg < nreg; ++gg) { ssz[gg].clear(); dsz[gg].clear(); }
+    std::vector<int32_t> ref, pslot;
+    for (int64_t w = 0; w < nw; ++w) {
+      while (w >= R->reg_wave[g + 1]) ++g;
+      const int32_t s0 = wave_first[w], cnt = wave_cnt[w];
+      int32_t K = 0;
+      for (int32_t i = 0; i < cnt; ++i) {
+        const int32_t r = slot_row[s0 + i];
+        K = std::max(K, dep_hi(r) - dep_lo(r));
+      }
+      // SoA block: header, r[], p0[], meta[], ref[K][], (factor) us[K][], pslot[]
+      ref.assign((size_t)K * cnt, 0);
+      pslot.clear();
+      const size_t base = W.size();
+      goff[w] = (int32_t)(base / 4);
+      W.resize(base + 4 + (size_t)3 * cnt, 0);
+      for (int32_t i = 0; i < cnt; ++i) {
+        const int32_t r = slot_row[s0 + i];
+        const int32_t lo = dep_lo(r), hi = dep_hi(r), nd = hi - lo;
+        int32_t nrem = 0;
+        for (int32_t p = lo; p < hi; ++p) {
+          const int32_t c = col[p];
+          int32_t v;
+          if (local(r, c, SC)) {
+            v = (slot_of[c] - reg_ptr[g]) % SC;
+          } else {
+            v = -(1 + (int32_t)pslot.size());
+            pslot.push_back(kind == 0 ? diag[c] : c);   // factor mailbox: diagonal position
+            ++nrem;
+          }
+          ref[(size_t)(p - lo) * cnt + i] = v;
+        }
+        R->ndeps_remote += nrem;
+        R->nrows_remote += nrem > 0;
+        W[base + 4 + i] = r;
+        W[base + 4 + cnt + i] = kind == 2 ? diag[r] : rs[r];
+        W[base + 4 + 2 * cnt + i] =
+            nd | (pub[r] ? 1 << 6 : 0) | (kind == 0 ? umask[r] << 7 : 0);
+      }
+      W[base + 0] = cnt;
+      W[base + 1] = s0 - reg_ptr[g];
+      W[base + 2] = K;
+      W[base + 3] = (int32_t)pslot.size();
+      W.insert(W.end(), ref.begin(), ref.end());
+      if (kind == 0) {
+        for (int32_t k = 0; k < K; ++k)
+          for (int32_t i = 0; i < cnt; ++i) W.push_back(us[(size_t)4 * slot_row[s0 + i] + k]);
+      }
+      W.insert(W.end(), pslot.begin(), pslot.end());
+      while ((W.size() - base) % 4) W.push_back(0);
+      // dynamic block: vals[NV][cnt] doubles, then 16-byte packets
+      //   factor: a_k (k < K), a_rr, u_k (k < K) [, norm];  fwd: b, l_k;
+      //   bwd: y, u_rr, u_k
+      const int32_t NV =
+          kind == 0 ? 2 * K + 1 + (tau_norms ? 1 : 0) : (kind == 1 ? K + 1 : K + 2);
+      sbytes[w] = (int32_t)(4 * (W.size() - base));
+      dbytes[w] = ((8 * NV * cnt + 15) & ~15) + 16 * (int32_t)pslot.size();
+      ssz[g].push_back(sbytes[w]);
+      dsz[g].push_back(dbytes[w]);
+    }
+  };
+  // slot ring and ring buffers: the largest prefetch distance D that fits,
+  // then the largest slot ring for it (a smaller ring sends far-back
+  // in-region dependencies through the mailbox, where the D-wave prefetch
+  // finds them long published)
+  auto fit = [&](int64_t SC, int32_t& D_, int32_t& cs_, int32_t& cd_) {
+    const int64_t fixed = 512 + 16 * (int64_t)R->max_waves + 8 * SC;
+    const int64_t ring = (smem_budget - fixed) & ~(int64_t)15;
+    if (ring < 1024) return false;
+    for (int D = 4; D >= 1; --D) {
+      const int32_t cd = min_cap(dsz, D, (int32_t)ring);
+      if (cd < 0) continue;
+      const int32_t cs = min_cap(ssz, 2 * D, (int32_t)(ring - cd));
+      if (cs < 0) continue;
+      D_ = D;
+      cs_ = cs;
+      cd_ = cd;
+      return true;
+    }
+    return false;
+  };
+  int64_t bestSC = 0;
+  int32_t bestD = 0;
+  for (int64_t SC = std::min<int64_t>(sc_need, 8192); SC >= 64; SC >>= 1) {
+    emit((int32_t)SC);
+    int32_t D = 0, cs = 0, cd = 0;
+    if (fit(SC, D, cs, cd) && D > bestD) {
+      bestD = D;
+      bestSC = SC;
+    }
+    if (bestD >= 3) break;
+  }
+  if (bestD == 0) return -2;
+  emit((int32_t)bestSC);
+  {
+    int32_t D = 0, cs = 0, cd = 0;
+    fit(bestSC, D, cs, cd);
+    R->S = 2 * D;
+    R->D = D;
+    R->CS = cs;
+    R->CD = cd;
+    R->SC = (int32_t)bestSC;
+  }
+  R->table.assign((size_t)4 * nw, 0);
+  std::vector<int32_t> so, dof;
+  for (int32_t gg = 0; gg < nreg; ++gg) {
+    ring_place(ssz[gg], R->CS, R->S, so);
+    ring_place(dsz[gg], R->CD, R->D, dof);
+    for (int32_t k = 0; k < R->reg_wave[gg + 1] - R->reg_wave[gg]; ++k) {
+      const int64_t w = R->reg_wave[gg] + k;
+      R->table[4 * w + 0] = goff[w];   // 16-byte units
+      R->table[4 * w + 1] = sbytes[w];
+      R->table[4 * w + 2] = so[k];
+      R->table[4 * w + 3] = dof[k];
+    }
+  }
+  sizes[0] = 4 * (int64_t)W.size();
+  sizes[1] = nw;
+  sizes[2] = nreg;
+  sizes[3] = R->SC;
+  sizes[4] = R->max_waves;
+  sizes[5] = R->S;
+  sizes[6] = R->D;
+  sizes[7] = R->CS;
+  sizes[8] = R->CD;
+  sizes[9] = R->ndeps_remote;
+  std::lock_guard<std::mutex> lk(g_rs_mu);
+  const int64_t h = g_rs_next++;
+  g_rs[h] = std::move(R);
+  return h;
+}
+
+// Copy a built stream out (host buffers sized from jv_rstream_build's
+// sizes) and release it.
+extern "C" int jv_rstream_export(int64_t handle, int32_t* words, int32_t* table,
+                                 int32_t* reg_wave) {
+  std::unique_ptr<RStream> R;
+  {
+    std::lock_guard<std::mutex> lk(g_rs_mu);
+    auto it = g_rs.find(handle);
+    if (it == g_rs.end()) return JV_EINVAL;
+    R = std::move(it->second);
+    g_rs.erase(it);
+  }
+  std::memcpy(words, R->words.data(), 4 * R->words.size());
+  std::memcpy(table, R->table.data(), 4 * R->table.size());
+  std::memcpy(reg_wave, R->reg_wave.data(), 4 * R->reg_wave.size());
+  return JV_OK;
+}

@@ -8,11 +8,12 @@ Index arrays on the device are int32 (checked), values float64.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
+from . import _lib, regionplan
 from ._lib import BackendUnavailable
 
 _INT32_MAX = 2**31 - 1
@@ -32,6 +33,11 @@ def torch():
         raise BackendUnavailable("no CUDA device: the ILU/stri/spmv path runs only on the GPU")
     _lib.load()
     return _torch
+
+
+def _hp(a):
+    """host numpy array -> ctypes pointer"""
+    return a.ctypes.data_as(ctypes.c_void_p)
 
 
 def stream():
@@ -345,7 +351,11 @@ class DevIlu:
         self._bwd = None
         self._fsched = None
         self._fsched_milu = None
-        self._rplan = None
+        self._regions = None
+        self._rstreams = {}
+        self._rchoice = {}
+        self.autotune_ms = {}
+        self._hpat = None
         self._elim = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
@@ -495,90 +505,154 @@ class DevIlu:
         _lib.call("jv_row_norms", self.n, ptr(self.row_start), ptr(self.val), self.tau,
                   ptr(self.norms), stream())
 
-    # CTA-resident region plan (stencil-class matrices) --------------------
-    # Regions must be convex in the dependency order (grid-aligned boxes for
-    # a stencil): the caller supplies them as a row -> region map (a domain
-    # decomposition, in the factor's row numbering).  Without one, BFS-grown
-    # regions are tried only when use_regions is set: they follow the level
-    # sets and come out as slabs, which serialise (slower than tickets).
-    use_regions = False
+    # CTA-resident region kernels ------------------------------------------
+    # One co-resident CTA per region of an acyclic box-like partition of the
+    # lower DAG (jv_region_partition_host); per sweep a wave stream
+    # (jv_rstream_build).  The factorization takes this path for
+    # stencil-class matrices (<= 4 pivots, pivots' U rows meeting the row
+    # only at its diagonal, no MILU), the solves for rows with <= 32
+    # dependencies; everything else runs the ticket kernels.  Both paths give
+    # the same bits.  JV_REGIONS=0 (or use_regions = False) turns it off.
+    # "auto": each sweep takes the faster of the two paths, timed once on
+    # first use (both give the same bits); "on" / "off" force it
+    region_mode = {"0": "off", "1": "on"}.get(os.environ.get("JV_REGIONS", ""), "auto")
+
+    @property
+    def use_regions(self):
+        return self.region_mode != "off"
+
+    @use_regions.setter
+    def use_regions(self, on):
+        self.region_mode = "on" if on else "off"
+
+    def _region_for(self, sweep):
+        """The region stream when the region path runs this sweep, else None."""
+        rp = self.region_stream(sweep)
+        if rp is None or self.region_mode == "on":
+            return rp
+        if sweep not in self._rchoice:
+            self._rchoice[sweep] = self._autotune(sweep, rp)
+        return rp if self._rchoice[sweep] else None
+
+    def _autotune(self, sweep, rp):
+        """Time the ticket and the region kernel of one sweep once each
+        (after a warm-up launch) and return True when the region one wins."""
+        t = torch()
+        ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
+        if sweep == "factor":
+            save = self.val.clone()
+            runs = [lambda: self._factor_tickets(0, self.n, 0, True),
+                    lambda: self._factor_region(rp, True)]
+        else:
+            which = 0 if sweep == "fwd" else 1
+            vin = t.ones(self.n, dtype=t.float64, device="cuda")
+            vout = t.empty_like(vin)
+            runs = [lambda: self._solve_tickets(which, vin, vout),
+                    lambda: self._region_run(rp, 1 + which, vin, vout, self.sbox)]
+        times = []
+        for k, fn in enumerate(runs):
+            for rep in range(2):
+                if sweep == "factor":
+                    self.val.copy_(save)
+                ev[2 * rep].record()
+                fn()
+                ev[2 * rep + 1].record()
+            t.cuda.synchronize()
+            times.append(ev[2].elapsed_time(ev[3]))
+        if sweep == "factor":
+            self.val.copy_(save)
+            _lib.call("jv_reset_row", ptr(self.err), stream())
+        check_hang()
+        self.autotune_ms[sweep] = tuple(times)
+        return times[1] < times[0]
+    region_min_rows = 64
     region_hint = None
+    KIND = {"factor": 0, "fwd": 1, "bwd": 2}
 
     def set_regions(self, region_of):
-        """Region id per row (factor numbering), ids 0..R-1 with R <= #SMs."""
+        """Caller-supplied partition: region id per row (factor numbering),
+        ids 0..R-1 with R <= #SMs (e.g. an application's domain decomposition)."""
         self.region_hint = np.ascontiguousarray(region_of, dtype=np.int32)
-        self._rplan = None
+        self._regions = None
+        self._rstreams = {}
+        self._rchoice = {}
 
-    def region_plan(self):
-        """Host-built region plan (jv_region_plan_host / jv_region_desc_host)
-        uploaded once; None when some row is not stencil-class."""
-        if self._rplan is None:
-            self._rplan = self._build_region_plan() or False
-        return self._rplan or None
+    def _host_pattern(self):
+        if self._hpat is None:
+            n = self.n
+            host = lambda x, m: np.ascontiguousarray(x[:m].cpu().numpy(), dtype=np.int32)
+            self._hpat = (host(self.row_start, n + 1), host(self.col, self.nnz),
+                          host(self.diag_pos, n))
+        return self._hpat
 
-    def _build_region_plan(self):
-        t = torch()
-        n = self.n
-        if n < 64:
-            return None
-        self.factor_schedule()
-        lib = _lib.load()
-        host = lambda x, m: np.ascontiguousarray(x[:m].cpu().numpy(), dtype=np.int32)
-        rs = host(self.row_start, n + 1)
-        col = host(self.col, self.nnz)
-        diag = host(self.diag_pos, n)
-        lev = host(self._fwd_levels, n)
-        sms = t.cuda.get_device_properties(t.cuda.current_device()).multi_processor_count
-        nreg = min(sms, max(1, n // 64))
+    def regions(self):
+        """(nreg, region_of) or None."""
+        if self._regions is None:
+            self._regions = self._partition() or False
+        return self._regions or None
+
+    def _partition(self):
         if self.region_hint is not None:
-            nreg = int(self.region_hint.max()) + 1
-        wave = lib.jv_region_threads()
-        region_of = (self.region_hint.copy() if self.region_hint is not None
-                     else np.full(n, -1, np.int32))
-        slot_row = np.empty(n, np.int32)
-        slot_of = np.empty(n, np.int32)
-        reg_ptr = np.empty(nreg + 1, np.int32)
-        wave_ptr = np.empty(nreg + 1, np.int32)
-        nlev = int(lev.max()) + 1
-        wave_beg = np.empty(n + nlev * nreg + 1, np.int32)
-        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
-        nw = lib.jv_region_plan_host(n, P(rs), P(col), P(lev), nreg, wave, P(region_of),
-                                     P(slot_row), P(slot_of), P(reg_ptr), P(wave_ptr), P(wave_beg))
-        if nw < 0:
+            return int(self.region_hint.max()) + 1, self.region_hint
+        rs, col, diag = self._host_pattern()
+        t = torch()
+        sms = t.cuda.get_device_properties(t.cuda.current_device()).multi_processor_count
+        return regionplan.partition(rs, col, diag, sms)
+
+    def region_stream(self, sweep):
+        """Device wave stream of one sweep ("factor", "fwd", "bwd") or None
+        when the region path does not apply."""
+        if not self.use_regions:
             return None
-        info = np.empty(n, np.int32)
-        drs = np.empty(n, np.int32)
-        ref = np.empty(4 * n, np.int32)
-        us = np.empty(4 * n, np.int32)
-        bad = lib.jv_region_desc_host(n, P(rs), P(col), P(diag), P(region_of), P(slot_row),
-                                      P(slot_of), P(reg_ptr), P(info), P(drs), P(ref), P(us))
-        if bad != 0:
+        if sweep not in self._rstreams:
+            self._rstreams[sweep] = self._build_rstream(sweep) or False
+            self._rchoice.pop(sweep, None)
+        return self._rstreams[sweep] or None
+
+    def _build_rstream(self, sweep):
+        if self.n < self.region_min_rows:
             return None
-        max_region = int(np.diff(reg_ptr).max())
-        if max_region * 8 > 220 * 1024:
+        if sweep == "factor" and self.milu:
             return None
-        up = lambda a: t.from_numpy(a).to("cuda")
-        return dict(nreg=nreg, max_region=max_region, slot_row=up(slot_row), info=up(info),
-                    drs=up(drs), ref=up(ref), us=up(us), reg_ptr=up(reg_ptr),
-                    wave_ptr=up(wave_ptr), wave_beg=up(wave_beg[:max(nw, 1)]),
-                    crossing=float(np.mean(ref[:n] < 0)))
+        reg = self.regions()
+        if reg is None:
+            return None
+        nreg, region_of = reg
+        rs, col, diag = self._host_pattern()
+        t = torch()
+        props = t.cuda.get_device_properties(t.cuda.current_device())
+        budget = props.shared_memory_per_block_optin - 2048   # static shared memory headroom
+        ws = regionplan.build_stream(sweep, rs, col, diag, region_of, nreg, budget, self.tau)
+        if ws is None:
+            return None
+        up = lambda a: t.from_numpy(np.ascontiguousarray(a)).to("cuda")
+        return dict(nreg=nreg, words=up(ws.words), table=up(ws.table), reg_wave=up(ws.reg_wave),
+                    slot_ring=ws.slot_ring, max_waves=ws.max_waves, S=ws.S, D=ws.D, CS=ws.CS,
+                    CD=ws.CD, waves=ws.waves, remote_deps=ws.remote_deps)
+
+    def _region_run(self, rp, kind, inp, out, box):
+        _lib.call("jv_region_run", kind, rp["nreg"], ptr(rp["words"]), ptr(rp["table"]),
+                  ptr(rp["reg_wave"]), rp["slot_ring"], rp["max_waves"], rp["S"], rp["D"],
+                  rp["CS"], rp["CD"], ptr(self.val), ptr(inp), ptr(out), ptr(self.norms),
+                  self.tau, ptr(box.buf), box.next_epoch(), ptr(self.err), stream())
 
     def factor_async(self, lo=0, hi=None, ready_below=0, norms=True):
         """Launch the factorization of rows [lo, hi) (all by default)."""
         hi = self.n if hi is None else hi
-        if (lo == 0 and hi == self.n and ready_below == 0 and not self.milu
-                and (self.use_regions or self.region_hint is not None)
-                and self.region_plan() is not None):
-            rp = self.region_plan()
-            if norms:
-                self.compute_norms()
-            _lib.call("jv_reset_row", ptr(self.err), stream())
-            _lib.call("jv_factor_regions", self.n, rp["nreg"], ptr(rp["slot_row"]),
-                      ptr(rp["info"]), ptr(rp["drs"]), ptr(rp["ref"]), ptr(rp["us"]),
-                      ptr(rp["reg_ptr"]), ptr(rp["wave_ptr"]), ptr(rp["wave_beg"]),
-                      rp["max_region"], ptr(self.val), ptr(self.norms), self.tau,
-                      ptr(self.fbox.buf), self.fbox.next_epoch(), ptr(self.err), stream())
-            return
+        if lo == 0 and hi == self.n and ready_below == 0:
+            rp = self._region_for("factor")
+            if rp is not None:
+                self._factor_region(rp, norms)
+                return
+        self._factor_tickets(lo, hi, ready_below, norms)
+
+    def _factor_region(self, rp, norms):
+        if norms and self.tau > 0:
+            self.compute_norms()
+        _lib.call("jv_reset_row", ptr(self.err), stream())
+        self._region_run(rp, 0, None, None, self.fbox)
+
+    def _factor_tickets(self, lo, hi, ready_below, norms):
         sched = self.factor_schedule()
         el = self.elim_lists()
         hub = self.hub_plans()
@@ -610,12 +684,19 @@ class DevIlu:
         return read_row_slot(slot)
 
     def solve_async(self, which, b, out):
+        rp = self._region_for("fwd" if which == 0 else "bwd")
+        if rp is not None:
+            self._region_run(rp, 1 + which, b, out, self.sbox)
+            return out
+        self._solve_tickets(which, b, out)
+        return out
+
+    def _solve_tickets(self, which, b, out):
         sched = self.fwd_schedule() if which == 0 else self.bwd_schedule()
         _lib.call("jv_solve", which, self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
                   ptr(self.diag_pos), ptr(sched.order), ptr(sched.batch_ptr), sched.nbatch,
                   ptr(b), ptr(out), ptr(self.sbox.buf), self.sbox.next_epoch(),
                   ctypes.c_void_p(self.ticket.data_ptr() + 8), stream())
-        return out
 
     def host_val(self):
         return host_f64(self.val, self.nnz)

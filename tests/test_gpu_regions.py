@@ -1,0 +1,101 @@
+"""GPU parity of the CTA-resident region kernels (csrc/region.cu): forced on,
+the factorization (stencil-class matrices) and both solves must equal the
+CPU oracle bit for bit, and the ticket kernels too; zero pivots are reported
+as the smallest row, as the reference does (factor.py:61-63)."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+jv = pytest.importorskip("paper_1812_06160_b200")
+from paper_1812_06160_b200 import device as dv  # noqa: E402
+from paper_1812_06160_b200 import workloads as W  # noqa: E402
+
+
+def _case(name):
+    return {
+        "poisson2d_48": (W.poisson2d(48), 0, 0.0),
+        "laplace7_20": (W.laplace7(20, 1), 0, 0.0),
+        "laplace7_20_tau": (W.laplace7(20, 2), 0, 0.05),
+        "convdiff3d_12_ilu1": (W.convdiff3d(12, 3), 1, 1e-3),
+        "stencil27_12": (W.stencil27(12, 4), 0, 0.0),
+        "random_dd_5000": (W.random_diag_dominant(5000, 7, seed=9), 0, 0.0),
+    }[name]
+
+
+NAMES = ["poisson2d_48", "laplace7_20", "laplace7_20_tau", "convdiff3d_12_ilu1",
+         "stencil27_12", "random_dd_5000"]
+
+
+def _front(a, k, tau):
+    fe = oracle.front_end(a.n, a.row_start, a.col, a.val, k=k, tau=tau)
+    return fe["row_start"], fe["col"], fe["diag"], fe["val"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("mode", ["on", "off", "auto"])
+def test_region_paths_bitwise(name, mode):
+    a, k, tau = _case(name)
+    rs, col, diag, val = _front(a, k, tau)
+    n = diag.size
+    want, bad = oracle.factor_serial(rs, col, val.copy(), diag, tau, False)
+    assert bad < 0
+    d = dv.DevIlu.from_host(n, rs, col, diag, val, tau=tau)
+    d.region_mode = mode
+    if mode == "on":
+        assert d.region_stream("fwd") is not None and d.region_stream("bwd") is not None
+        stencil = name.startswith(("poisson", "laplace"))
+        assert (d.region_stream("factor") is not None) == stencil
+    assert d.factor() == -1
+    assert np.array_equal(d.host_val(), want)
+    b = np.random.default_rng(1).uniform(-1, 1, n)
+    y = dv.empty_f64(n)
+    x = dv.empty_f64(n)
+    for rep in range(2):   # mailbox epochs advance between calls
+        d.solve_async(0, dv.f64(b), y)
+        d.solve_async(1, y, x)
+        yo = oracle.solve_forward(rs, col, want, b)
+        xo, _ = oracle.solve_backward(rs, col, want, diag, yo)
+        assert np.array_equal(dv.host_f64(y, n), yo)
+        assert np.array_equal(dv.host_f64(x, n), xo)
+    dv.check_hang()
+
+
+def test_region_factor_zero_pivot_smallest_row():
+    """A zero pivot in the middle of a stencil matrix: the region factor
+    reports the smallest bad row, like the reference."""
+    a = W.poisson2d(40)
+    rs, col, diag, val = _front(a, 0, 0.0)
+    n = diag.size
+    val = val.copy()
+    # make two rows singular after elimination: zero their diagonal and
+    # their strictly-lower entries
+    for r in (900, 1300):
+        val[rs[r]:diag[r] + 1] = 0.0
+    want, bad = oracle.factor_serial(rs, col, val.copy(), diag, 0.0, False)
+    assert bad == 900
+    d = dv.DevIlu.from_host(n, rs, col, diag, val)
+    d.region_mode = "on"
+    assert d.region_stream("factor") is not None
+    assert d.factor() == 900
+    got = d.host_val()
+    upto = rs[bad + 1]
+    assert np.array_equal(got[:upto], want[:upto])
+
+
+def test_region_many_epochs():
+    """Repeated launches (epochs) on one plan stay bitwise and never hang."""
+    a = W.laplace7(16, 5)
+    rs, col, diag, val = _front(a, 0, 0.0)
+    n = diag.size
+    want, _ = oracle.factor_serial(rs, col, val.copy(), diag, 0.0, False)
+    d = dv.DevIlu.from_host(n, rs, col, diag, val)
+    d.region_mode = "on"
+    for _ in range(20):
+        dv.upload_f64(d.val, val)
+        assert d.factor() == -1
+    assert np.array_equal(d.host_val(), want)
+    dv.check_hang()
