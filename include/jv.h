@@ -297,9 +297,10 @@ int jv_classify_solve(int which, int32_t n, const int32_t* row_start, const int3
  *   jv_region_partition_host  region id per row (returns #regions or -1);
  *   jv_rstream_build          wave stream of one direction (kind 0 factor of
  *                             a stencil-class matrix, 1 forward, 2 backward);
- *                             sizes[10] = {static bytes, waves, nreg,
- *                             max_region, max_waves, S, D, CS, CD, remote
- *                             deps}; returns a handle > 0, -1 (a row does not
+ *                             sizes[11] = {static bytes, waves, nreg,
+ *                             slot ring, max_waves, S, D, CS, CD, remote
+ *                             deps, packed values, packed vector};
+ *                             returns a handle > 0, -1 (a row does not
  *                             qualify) or -2 (shared memory too small);
  *   jv_rstream_export         copies the stream out and frees the handle.
  * jv_region_run replaces factor_serial_kernel (_kernels.py:197-204) for
@@ -311,7 +312,10 @@ int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* row_start_h,
                          const int32_t* col_h, const int32_t* diag_h, const int32_t* region_of_h,
                          int32_t nreg, int32_t threads, int64_t smem_budget, int32_t tau_norms,
                          int64_t* sizes_h);
-int jv_rstream_export(int64_t handle, int32_t* words_h, int32_t* table_h, int32_t* reg_wave_h);
+int jv_rstream_export(int64_t handle, int32_t* words_h, int32_t* table_h, int32_t* reg_wave_h,
+                      int32_t* sidx_h, int32_t* vidx_h);
+/* dst[e] = src[sidx[e]] (0 where sidx < 0): a sweep's wave-ordered values */
+int jv_pack_values(int64_t m, const int32_t* sidx, const double* src, double* dst, void* stream);
 int jv_region_threads(void);
 /* diagnostic switches of the region kernels (bit 0: proxy fence before each
  * static bulk copy, bit 1: no late mailbox re-probes) */
@@ -319,7 +323,8 @@ int jv_set_region_flags(unsigned flags);
 int64_t jv_region_smem_fixed(int32_t max_region, int32_t max_waves);
 int jv_region_run(int32_t kind, int32_t nreg, const void* words, const int32_t* table,
                   const int32_t* reg_wave, int32_t max_region, int32_t max_waves, int32_t S,
-                  int32_t D, int32_t CS, int32_t CD, double* val, const double* in, double* out,
+                  int32_t D, int32_t CS, int32_t CD, double* val, const double* pack,
+                  const double* vpack, double* out,
                   const double* norms, double tau, uint64_t* mbox, uint32_t epoch,
                   int32_t* err_row, void* stream);
 

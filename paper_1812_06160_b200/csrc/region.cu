@@ -41,14 +41,17 @@ namespace jvr {
 
 constexpr int kThreads = 512;   // rows per wave (compute threads)
 constexpr int kNB = 16;   // static-block mbarriers in the ring (S + 1 <= kNB)
+constexpr int kL2 = 12;   // waves of L2 bulk prefetch ahead of the gathers
 
 struct RArgs {
   const int4* words;   // static stream, 16-byte units
-  const int4* table;   // per wave {block offset (16 B units), bytes, ring offset, dyn offset}
+  const int4* table;   // 2 per wave: {block (16 B units), bytes, ring off, dyn off},
+                       // {packed values (16 B units), bytes, 0, 0}
   const int32_t* reg_wave;
   int32_t SC, max_waves, S, D, CS, CD;   // SC: slot ring (power of 2)
   double* val;
-  const double* in;
+  const double* pack;   // matrix values packed in wave order (jv_pack_values)
+  const double* vpack;  // per-call vector packed in wave order
   double* out;
   const double* norms;
   double tau;
@@ -77,22 +80,6 @@ JV_INLINE void bar_wait(uint64_t* b, uint32_t parity) {
       "RW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra RW_%=;\n}" ::"r"(sa(b)), "r"(parity) : "memory");
 }
-JV_INLINE void cp8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa(dst)), "l"(src) : "memory");
-}
-JV_INLINE void cp16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(dst)), "l"(src) : "memory");
-}
-JV_INLINE void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-JV_INLINE void cp_wait_pending(int n) {
-  switch (n) {
-    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-  }
-}
-
 // wave block view (regions_host.cpp): SoA arrays of cnt rows
 struct Wave {
   const int32_t* b;
@@ -111,50 +98,23 @@ struct Wave {
   template <int KIND>
   JV_INLINE int pslot(int j) const { return b[4 + (3 + (KIND == 0 ? 2 * K : K)) * cnt + j]; }
 };
-// values per row in the dynamic block
-template <int KIND>
-JV_INLINE int nvals(int K, bool tau) {
-  return KIND == 0 ? 2 * K + 1 + (tau ? 1 : 0) : (KIND == 1 ? K + 1 : K + 2);
-}
-
 constexpr int kCompute = 512;
-constexpr int kProducers = 128;   // producer threads (4 warps)
-constexpr int kBlock = kCompute + kProducers;
+constexpr int kBlock = kCompute + 64;   // + a producer warp (one lane) and a prober warp
+constexpr int kWin = 8;                 // prober window (waves)
 
-// Gathers of wave t by the producer warp: lane l fetches the values of rows
-// l, l + 32, ... into column i of vals[NV][cnt] and the wave's mailbox
-// packets; completion is signalled per lane with cp.async.mbarrier.arrive.
-template <int KIND>
-JV_INLINE void gather_wave(const RArgs& A, const int4& t, const unsigned char* sring,
-                           unsigned char* dring, bool tau, int lane) {
-  const Wave V(sring + t.z);
-  double* vals = reinterpret_cast<double*>(dring + t.w);
-  const int cnt = V.cnt, K = V.K;
-  if (!(jv::g_region_flags & 4)) {
-    for (int i = lane; i < cnt; i += kProducers) {
-      const int p0 = V.p0(i);
-      const int nd = V.meta(i) & 63;
-      if (KIND == 0) {
-        for (int k = 0; k < nd; ++k) cp8(vals + k * cnt + i, A.val + p0 + k);
-        cp8(vals + K * cnt + i, A.val + p0 + nd);
-        for (int k = 0; k < nd; ++k) cp8(vals + (K + 1 + k) * cnt + i, A.val + V.us(k, i));
-        if (tau) cp8(vals + (2 * K + 1) * cnt + i, A.norms + V.row(i));
-      } else if (KIND == 1) {
-        cp8(vals + i, A.in + V.row(i));
-        for (int k = 0; k < nd; ++k) cp8(vals + (1 + k) * cnt + i, A.val + p0 + k);
-      } else {
-        cp8(vals + i, A.in + V.row(i));
-        for (int k = 0; k <= nd; ++k) cp8(vals + (1 + k) * cnt + i, A.val + p0 + k);
-      }
-    }
-  }
-  unsigned char* pk = dring + t.w + ((8 * nvals<KIND>(K, tau) * cnt + 15) & ~15);
-  for (int j = lane; j < V.NP; j += kProducers)
-    cp16(pk + 16 * j, A.mbox + 2 * (int64_t)V.pslot<KIND>(j));
+JV_INLINE void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(dst)), "l"(src) : "memory");
+}
+JV_INLINE bool bar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(sa(b)), "r"(parity) : "memory");
+  return ok != 0;
 }
 
-JV_INLINE void cp_arrive(uint64_t* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sa(b)) : "memory");
+JV_INLINE void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 JV_INLINE int ld_volatile_shared(const int* p) {
   int v;
@@ -162,144 +122,193 @@ JV_INLINE int ld_volatile_shared(const int* p) {
   return v;
 }
 
-// Warp-specialised: warps 0..15 compute (one row per thread, a named
-// barrier per wave), warp 16 produces — bulk copies of the static blocks
-// (TMA, mbarrier complete_tx) and cp.async gathers of the values (mbarrier
-// arrive per lane), running up to D waves ahead of the compute warps, whose
-// progress it reads from a shared counter before reusing ring space.
-
+// Warp-specialised CTA: warps 0..15 compute (one row per thread, a named
+// barrier per wave); one lane of warp 16 produces.  Per wave the producer
+// issues three bulk copies (TMA, cp.async.bulk + mbarrier complete_tx): the
+// static block, the packed matrix values and the packed per-call vector,
+// all addressed from the wave table alone, up to D waves ahead of the
+// compute warps (whose progress it reads from a shared counter before
+// reusing ring space), with L2 bulk prefetches kL2 waves further ahead.
 template <int KIND>
 __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
   extern __shared__ __align__(128) unsigned char rsm[];
   const unsigned full = 0xffffffffu;
   const int tid = threadIdx.x;
-  uint64_t* sbar = reinterpret_cast<uint64_t*>(rsm);          // static full [kNB]
-  uint64_t* dbar = sbar + kNB;                                 // dynamic full [kNB]
-  int* done = reinterpret_cast<int*>(rsm + 2 * 8 * kNB);      // waves finished
-  int4* tab = reinterpret_cast<int4*>(rsm + 512);
-  double* slot = reinterpret_cast<double*>(rsm + 512 + 16 * A.max_waves);
-  unsigned char* sring = rsm + 512 + 16 * A.max_waves + 8 * A.SC;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rsm);            // wave full [kNB]
+  int* done = reinterpret_cast<int*>(rsm + 8 * kNB);          // waves finished
+  int* probed = done + 1;                                       // waves whose remote deps are in
+  int4* tab = reinterpret_cast<int4*>(rsm + 256);             // 2 per wave
+  double* slot = reinterpret_cast<double*>(rsm + 256 + 32 * A.max_waves);
+  unsigned char* sring = rsm + 256 + 32 * A.max_waves + 8 * A.SC;
   unsigned char* dring = sring + A.CS;
   const int w0 = A.reg_wave[blockIdx.x];
   const int nw = A.reg_wave[blockIdx.x + 1] - w0;
-  for (int i = tid; i < nw; i += blockDim.x) tab[i] = A.table[w0 + i];
+  for (int i = tid; i < 2 * nw; i += blockDim.x) tab[i] = A.table[2 * w0 + i];
   if (tid == 0) {
-    for (int b = 0; b < kNB; ++b) {
-      bar_init(&sbar[b], 1);
-      bar_init(&dbar[b], kProducers);
-    }
+    for (int b = 0; b < kNB; ++b) bar_init(&bar[b], 1);
     *done = 0;
+    *probed = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int S = A.S, D = A.D;
+  const int D = A.D;
   const bool tau = KIND == 0 && A.tau > 0.0;
   const unsigned flags = jv::g_region_flags;
 
-  if (tid >= kCompute) {
-    // ------------------------------------------------------------ producer
-    const int lane = tid - kCompute;
-    int sx = 0;   // next static block to issue
-    for (int x = 0; x < nw; ++x) {
-      // static blocks up to x + (S - D): block y may overlap block y - S - 1
-      for (; sx < nw && sx <= x + (S - D); ++sx) {
-        while (ld_volatile_shared(done) < sx - S) __nanosleep(32);
+  if (tid >= kCompute + 32) {
+    // -------------------------------------------------------------- prober
+    // Fetches the mailbox packets of the remote dependencies of the next
+    // kWin waves, round after round: each round copies every still-stale
+    // packet of the window (cp.async, all in flight together, one round
+    // trip), then checks the epochs in shared memory; the window's first
+    // wave is released to the compute warps (`probed`) once all of its
+    // packets are current.  Decoupled from the compute warps' barrier
+    // cadence, so a value published upstream reaches a waiting wave within
+    // about one round trip, and values published earlier cost nothing.
+    const int lane = tid - kCompute - 32;
+    auto pkts = [&](int x) -> unsigned char* {
+      const int4 v = tab[2 * x + 1];
+      return dring + tab[2 * x].w + v.y + v.w;
+    };
+    auto fresh = [&](const unsigned char* p) {
+      const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(p);
+      return (uint32_t)(q.x >> 32) == A.epoch && (uint32_t)(q.y >> 32) == A.epoch;
+    };
+    int lo = 0, hi = 0;
+    unsigned ns = 0, spins = 0;
+    while (lo < nw) {
+      // admit waves whose blocks are in (non-blocking)
+      while (hi < nw && hi < lo + kWin && bar_test(&bar[hi % kNB], (uint32_t)((hi / kNB) & 1))) {
+        const Wave X(sring + tab[2 * hi].z);
+        unsigned char* pk = pkts(hi);
+        for (int j = lane; j < X.NP; j += 32)
+          *reinterpret_cast<ulonglong2*>(pk + 16 * j) = make_ulonglong2(0ull, 0ull);
+        ++hi;
+      }
+      __syncwarp();
+      // one round: copy every stale packet of the window
+      bool issued = false;
+      for (int x = lo; x < hi; ++x) {
+        const Wave X(sring + tab[2 * x].z);
+        unsigned char* pk = pkts(x);
+        for (int j = lane; j < X.NP; j += 32)
+          if (!fresh(pk + 16 * j) && !(flags & 8)) {
+            cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot<KIND>(j));
+            issued = true;
+          }
+      }
+      asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      // release the leading waves that are complete
+      const int lo0 = lo;
+      while (lo < hi) {
+        const Wave X(sring + tab[2 * lo].z);
+        const unsigned char* pk = pkts(lo);
+        bool ok = true;
+        for (int j = lane; j < X.NP; j += 32) ok = ok && ((flags & 8) || fresh(pk + 16 * j));
+        if (!__all_sync(full, ok)) break;
+        ++lo;
+      }
+      if (lo != lo0) {
         if (lane == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          const int4 t = tab[sx];
-          uint64_t* b = &sbar[sx % kNB];
-          bar_expect_tx(b, (uint32_t)t.y);
-          bulk_g2s(sring + t.z, A.words + t.x, (uint32_t)t.y, b);
+          __threadfence_block();
+          asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(probed)), "r"(lo) : "memory");
+        }
+        ns = 0;
+        spins = 0;
+      } else if (!__any_sync(full, issued) || hi == lo) {
+        // nothing in flight: wait for the producer (or a slow upstream)
+        if (ns) __nanosleep(ns);
+        ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
+        if (++spins == jv::g_spin_limit) {
+          atomicExch(&jv::g_hang, 1);
+          if (lane == 0)
+            asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(probed)), "r"(nw) : "memory");
+          break;
         }
       }
-      // dynamic block x may overlap block x - D - 1
-      while (ld_volatile_shared(done) < x - D) __nanosleep(32);
-      bar_wait(&sbar[x % kNB], (uint32_t)((x / kNB) & 1));
-      gather_wave<KIND>(A, tab[x], sring, dring, tau, lane);
-      cp_arrive(&dbar[x % kNB]);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  if (tid >= kCompute) {
+    // ------------------------------------------------------------ producer
+    if (tid != kCompute) return;
+    auto prefetch = [&](int x) {
+      const int4 t2 = tab[2 * x], v2 = tab[2 * x + 1];
+      l2_prefetch_bulk(A.words + t2.x, (uint32_t)t2.y);
+      if (v2.y > 0) l2_prefetch_bulk(A.pack + 2 * (int64_t)v2.x, (uint32_t)v2.y);
+      if (v2.w > 0) l2_prefetch_bulk(A.vpack + 2 * (int64_t)v2.z, (uint32_t)v2.w);
+    };
+    for (int x = 0; x < kL2 && x < nw; ++x) prefetch(x);
+    for (int x = 0; x < nw; ++x) {
+      if (x + kL2 < nw) prefetch(x + kL2);
+      // ring blocks of wave x may overlap those of wave x - D - 1
+      while (ld_volatile_shared(done) < x - D) __nanosleep(20);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int4 t = tab[2 * x], v = tab[2 * x + 1];
+      uint64_t* b = &bar[x % kNB];
+      const bool skip = flags & 4;   // diagnostic: no value copies (wrong results)
+      bar_expect_tx(b, (uint32_t)(t.y + (skip ? 0 : v.y + v.w)));
+      bulk_g2s(sring + t.z, A.words + t.x, (uint32_t)t.y, b);
+      unsigned char* blk = dring + t.w;
+      if (!skip && v.y > 0) bulk_g2s(blk, A.pack + 2 * (int64_t)v.x, (uint32_t)v.y, b);
+      if (!skip && v.w > 0) bulk_g2s(blk + v.y, A.vpack + 2 * (int64_t)v.z, (uint32_t)v.w, b);
+    }
     return;
   }
 
   // -------------------------------------------------------------- compute
+  constexpr int kR = 4;   // register fast path: dependencies per row
   const jv::Trace T = jv::trace_begin();
   for (int w = 0; w < nw; ++w) {
     if (tid == 0) jv::trace_mark(T, w0 + w, 1);
-    bar_wait(&dbar[w % kNB], (uint32_t)((w / kNB) & 1));
-    bar_wait(&sbar[w % kNB], (uint32_t)((w / kNB) & 1));
-    const int4 t = tab[w];
+    bar_wait(&bar[w % kNB], (uint32_t)((w / kNB) & 1));
+    const int4 t = tab[2 * w];
+    const int4 tv = tab[2 * w + 1];
     const Wave V(sring + t.z);
     const int cnt = V.cnt, K = V.K;
     const bool active = tid < cnt;
     const double* vals = reinterpret_cast<const double*>(dring + t.w);
-    unsigned char* pk = dring + t.w + ((8 * nvals<KIND>(K, tau) * cnt + 15) & ~15);
+    const double* vec = reinterpret_cast<const double*>(dring + t.w + tv.y);
+    const unsigned char* pk = dring + t.w + tv.y + tv.w;
+    auto val = [&](int k) -> double { return vals[k * cnt + tid]; };
+    auto packet = [&](int j) -> double {
+      const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(pk + 16 * j);
+      return __longlong_as_double((long long)((p.x & 0xffffffffull) | (p.y << 32)));
+    };
+    if (tid == 0) jv::trace_mark(T, w0 + w, 2);
+    // the prober has this wave's remote dependencies (every wave passes
+    // through the prober, so it never looks at a ring block already reused)
+    while (ld_volatile_shared(probed) <= w) {
+    }
+    __threadfence_block();
+    double dv[kR];
     int nd = 0, meta = 0;
-    unsigned miss = 0;   // bit k: dependency k still unpublished
     if (active) {
       meta = V.meta(tid);
       nd = meta & 63;
-      for (int k = 0; k < nd; ++k) {
-        const int ref = V.ref(k, tid);
-        if (ref < 0) {
-          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(pk + 16 * (-1 - ref));
-          if ((uint32_t)(p.x >> 32) != A.epoch || (uint32_t)(p.y >> 32) != A.epoch)
-            miss |= 1u << k;
-        }
-      }
-    }
-    if (tid == 0) jv::trace_mark(T, w0 + w, 2);
-    // dependencies not yet published when prefetched: warp-converged live
-    // probes (no lane spins alone); a hit is written back into the packet
-    if (flags & 8) miss = 0;   // diagnostic: no waiting (wrong results)
-    if (__any_sync(full, miss)) {
-      unsigned ns = 0, spins = 0;
-      while (__any_sync(full, miss)) {
-        unsigned m = miss;
-        while (m) {
-          const int k = __ffs(m) - 1;
-          m &= m - 1;
-          const int j = -1 - V.ref(k, tid);
-          unsigned long long x0, x1;
-          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
-                       : "=l"(x0), "=l"(x1)
-                       : "l"(A.mbox + 2 * (int64_t)V.pslot<KIND>(j)) : "memory");
-          if ((uint32_t)(x0 >> 32) == A.epoch && (uint32_t)(x1 >> 32) == A.epoch) {
-            *reinterpret_cast<ulonglong2*>(pk + 16 * j) = make_ulonglong2(x0, x1);
-            miss &= ~(1u << k);
-          }
-        }
-        if (__any_sync(full, miss)) {
-          if (ns) __nanosleep(ns);
-          ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
-          if (++spins == jv::g_spin_limit) {
-            atomicExch(&jv::g_hang, 1);
-            break;
-          }
+#pragma unroll
+      for (int k = 0; k < kR; ++k) {
+        dv[k] = 1.0;
+        if (k < nd) {
+          const int ref = V.ref(k, tid);
+          dv[k] = ref >= 0 ? slot[ref] : packet(-1 - ref);
         }
       }
     }
     if (tid == 0) jv::trace_mark(T, w0 + w, 3);
     if (active) {
       const int me = (V.slot0 + tid) & (A.SC - 1);
-      auto dep = [&](int k) -> double {
-        const int ref = V.ref(k, tid);
-        if (ref >= 0) return slot[ref];
-        const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(pk + 16 * (-1 - ref));
-        return __longlong_as_double((long long)((p.x & 0xffffffffull) | (p.y << 32)));
-      };
-      auto val = [&](int k) -> double { return vals[k * cnt + tid]; };
       const int p0 = V.p0(tid);
       if (KIND == 0) {
-        double a[4], d4[4], u[4], l[4];
+        double a[4], u[4], l[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           a[k] = k < nd ? val(k) : 0.0;
-          d4[k] = k < nd ? dep(k) : 1.0;
           u[k] = k < nd ? val(K + 1 + k) : 0.0;
         }
-        jv::ddiv_batch<4>(a, d4, l, nd);
-        const double thresh = tau ? jv::dmul(A.tau, val(2 * K + 1)) : 0.0;
+        jv::ddiv_batch<4>(a, dv, l, nd);
+        const double thresh = tau ? jv::dmul(A.tau, vec[tid]) : 0.0;
         double d = val(K);
         const int umask = (meta >> 7) & 15;
 #pragma unroll
@@ -311,22 +320,27 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
         }
         slot[me] = d;
         if (meta & 64) jv::mbox_put(A.mbox, p0 + nd, d, A.epoch);
-        if (!(flags & 16)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k < nd) __stcg(A.val + p0 + k, l[k]);
-          __stcg(A.val + p0 + nd, d);
-        }
+        for (int k = 0; k < 4; ++k)
+          if (k < nd) __stcg(A.val + p0 + k, l[k]);
+        __stcg(A.val + p0 + nd, d);
         if (d == 0.0) atomicMin(A.err, V.row(tid));
       } else {
-        const int o = KIND == 1 ? 1 : 2;
-        double sacc = val(0);
-        for (int k = 0; k < nd; ++k) sacc = jv::dsub(sacc, jv::dmul(val(o + k), dep(k)));
-        if (KIND == 2) sacc = jv::ddiv(sacc, val(1));
+        const int o = KIND == 1 ? 0 : 1;
+        double sacc = vec[tid];
+#pragma unroll
+        for (int k = 0; k < kR; ++k)
+          if (k < nd) sacc = jv::dsub(sacc, jv::dmul(val(o + k), dv[k]));
+        for (int k = kR; k < nd; ++k) {
+          const int ref = V.ref(k, tid);
+          const double x = ref >= 0 ? slot[ref] : packet(-1 - ref);
+          sacc = jv::dsub(sacc, jv::dmul(val(o + k), x));
+        }
+        if (KIND == 2) sacc = jv::ddiv(sacc, val(0));
         slot[me] = sacc;
         const int r = V.row(tid);
         if (meta & 64) jv::mbox_put(A.mbox, r, sacc, A.epoch);
-        if (!(flags & 16)) __stcg(A.out + r, sacc);
+        __stcg(A.out + r, sacc);
       }
     }
     if (tid == 0) jv::trace_mark(T, w0 + w, 4);
@@ -340,6 +354,29 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
 
 }  // namespace jvr
 
+namespace jvr {
+__global__ void pack_kernel(int64_t m, const int32_t* __restrict__ sidx, const double* __restrict__ src,
+                            double* __restrict__ dst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = __ldcs(sidx + e);
+    __stcs(dst + e, k >= 0 ? __ldg(src + k) : 0.0);
+  }
+}
+}  // namespace jvr
+
+// dst[e] = src[sidx[e]] (0 where sidx < 0): the wave-ordered value arrays
+// of the region kernels, refreshed once per factorization
+extern "C" int jv_pack_values(int64_t m, const int32_t* sidx, const double* src, double* dst,
+                              void* stream) {
+  if (m <= 0) return JV_OK;
+  int64_t grid = (m + 255) / 256;
+  if (grid > 8 * jvh::sm_count()) grid = 8 * jvh::sm_count();
+  jvr::pack_kernel<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(m, sidx, src, dst);
+  JV_CHECK_LAUNCH("jv_pack_values");
+  return JV_OK;
+}
+
 extern "C" int jv_region_threads(void) { return jvr::kThreads; }
 
 extern "C" int jv_set_region_flags(unsigned flags) {
@@ -349,15 +386,15 @@ extern "C" int jv_set_region_flags(unsigned flags) {
 }
 
 extern "C" int64_t jv_region_smem_fixed(int32_t slot_ring, int32_t max_waves) {
-  return 512 + 16 * (int64_t)max_waves + 8 * (int64_t)slot_ring;
+  return 256 + 32 * (int64_t)max_waves + 8 * (int64_t)slot_ring;
 }
 
 extern "C" int jv_region_run(int32_t kind, int32_t nreg, const void* words, const int32_t* table,
                              const int32_t* reg_wave, int32_t slot_ring, int32_t max_waves,
                              int32_t S, int32_t D, int32_t CS, int32_t CD, double* val,
-                             const double* in, double* out, const double* norms, double tau,
+                             const double* pack, const double* vpack, double* out, const double* norms, double tau,
                              uint64_t* mbox, uint32_t epoch, int32_t* err_row, void* stream) {
-  if (kind < 0 || kind > 2 || nreg < 1 || epoch == 0 || D < 1 || D > 4 || S < D ||
+  if (kind < 0 || kind > 2 || nreg < 1 || epoch == 0 || D < 1 || D > 12 || S < D ||
       slot_ring < 1 || (slot_ring & (slot_ring - 1)) ||
       S + 1 > jvr::kNB) {
     jvh::set_error("jv_region_run: bad argument (kind=%d nreg=%d S=%d D=%d)", kind, nreg, S, D);
@@ -378,7 +415,7 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, const void* words, cons
     return JV_ECOOP;
   }
   jvr::RArgs A{reinterpret_cast<const int4*>(words), reinterpret_cast<const int4*>(table),
-               reg_wave, slot_ring, max_waves, S, D, CS, CD, val, in, out, norms, tau, mbox,
+               reg_wave, slot_ring, max_waves, S, D, CS, CD, val, pack, vpack, out, norms, tau, mbox,
                epoch, err_row};
   void* args[] = {&A};
   e = cudaLaunchCooperativeKernel(fn, dim3(nreg), dim3(jvr::kBlock), args, smem,

@@ -170,7 +170,9 @@ struct RStream {
   int32_t nreg = 0, max_region = 0, max_waves = 0;
   int32_t S = 0, D = 0, CS = 0, CD = 0, SC = 0;
   std::vector<int32_t> words;     // static stream (16-byte aligned blocks)
-  std::vector<int32_t> table;     // int4 per wave {goff16, bytes, soff, doff}
+  std::vector<int32_t> table;     // 8 ints per wave {goff16, bytes, soff, doff, voff16, vbytes, 0, 0}
+  std::vector<int32_t> sidx;      // packed value -> source position in val (-1: padding)
+  std::vector<int32_t> vidx;      // packed per-call vector -> row (-1: padding)
   std::vector<int32_t> reg_wave;  // nreg + 1
   int64_t nrows_remote = 0, ndeps_remote = 0;
 };
@@ -228,9 +230,9 @@ int32_t min_cap(const std::vector<std::vector<int32_t>>& per_region, int window,
 // <= 4 pivots, every pivot's U row meets the row only at its diagonal),
 // 1: forward solve (unit L), 2: backward solve.  threads = rows per wave,
 // smem_budget = shared memory the kernel may use (bytes), tau_norms = the
-// factor gathers each row's norm (tau > 0).  sizes[0..9] receive
-// {static bytes, total waves, nreg, max_region, max_waves, S, D, CS, CD,
-// remote-dependency count}.  Returns a handle > 0, or
+// factor gathers each row's norm (tau > 0).  sizes[0..11] receive
+// {static bytes, total waves, nreg, slot ring, max_waves, S, D, CS, CD,
+// remote-dependency count, packed values, packed vector}.  Returns a handle > 0, or
 // -1 (a row does not qualify), -2 (does not fit in shared memory).
 extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, const int32_t* col,
                                     const int32_t* diag, const int32_t* region_of, int32_t nreg,
@@ -337,7 +339,11 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   int64_t sc_need = 64;
   while (sc_need < need) sc_need <<= 1;
   std::vector<char> pub(n, 0);
-  std::vector<int32_t> goff(nw), sbytes(nw), dbytes(nw);
+  std::vector<int32_t> goff(nw), sbytes(nw), dbytes(nw), voff(nw), vbytes(nw);
+  std::vector<int32_t>& sidx = R->sidx;
+  std::vector<int32_t>& vidx = R->vidx;
+  std::vector<int32_t> coff(nw), cbytes(nw);
+  int64_t vtot = 0, ctot = 0;
   std::vector<std::vector<int32_t>> ssz(nreg), dsz(nreg);
   std::vector<int32_t>& W = R->words;
   auto local = [&](int32_t r, int32_t c, int32_t SC) {
@@ -355,6 +361,10 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
     int32_t g = 0;
     for (int32_t gg = 0; gg < nreg; ++gg) { ssz[gg].clear(); dsz[gg].clear(); }
     std::vector<int32_t> ref, pslot;
+    sidx.clear();
+    vidx.clear();
+    vtot = 0;
+    ctot = 0;
     for (int64_t w = 0; w < nw; ++w) {
       while (w >= R->reg_wave[g + 1]) ++g;
       const int32_t s0 = wave_first[w], cnt = wave_cnt[w];
@@ -403,13 +413,46 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       }
       W.insert(W.end(), pslot.begin(), pslot.end());
       while ((W.size() - base) % 4) W.push_back(0);
-      // dynamic block: vals[NV][cnt] doubles, then 16-byte packets
-      //   factor: a_k (k < K), a_rr, u_k (k < K) [, norm];  fwd: b, l_k;
-      //   bwd: y, u_rr, u_k
-      const int32_t NV =
-          kind == 0 ? 2 * K + 1 + (tau_norms ? 1 : 0) : (kind == 1 ? K + 1 : K + 2);
+      // values of the wave, packed once per factorization into a global
+      // array in wave order (vals[NVm][cnt], jv_pack_values with sidx) and
+      // bulk-copied: factor: a_k (k < K), a_rr, u_k (k < K);  fwd: l_k;
+      // bwd: u_rr, u_k.  The per-call vector (fwd b, bwd y; factor norms
+      // when tau > 0) is gathered per row behind them, then the packets.
+      const int32_t NVm = kind == 0 ? 2 * K + 1 : (kind == 1 ? K : K + 1);
+      const bool vec = kind != 0 || tau_norms;
+      const int32_t vb = (8 * NVm * cnt + 15) & ~15;
+      voff[w] = vtot / 16;
+      vbytes[w] = vb;
+      vtot += vb;
+      const size_t s0x = sidx.size();
+      sidx.resize(s0x + vb / 8, -1);
+      for (int32_t i = 0; i < cnt; ++i) {
+        const int32_t r = slot_row[s0 + i];
+        const int32_t nd = dep_hi(r) - dep_lo(r);
+        auto put = [&](int32_t k, int32_t src) { sidx[s0x + (size_t)k * cnt + i] = src; };
+        if (kind == 0) {
+          for (int32_t k = 0; k < nd; ++k) put(k, rs[r] + k);
+          put(K, rs[r] + nd);
+          for (int32_t k = 0; k < nd; ++k) put(K + 1 + k, us[(size_t)4 * r + k]);
+        } else if (kind == 1) {
+          for (int32_t k = 0; k < nd; ++k) put(k, rs[r] + k);
+        } else {
+          for (int32_t k = 0; k <= nd; ++k) put(k, diag[r] + k);
+        }
+      }
+      // the per-call vector in wave order (jv_pack_values with vidx)
+      const int32_t cb = vec ? (8 * cnt + 15) & ~15 : 0;
+      coff[w] = ctot / 16;
+      cbytes[w] = cb;
+      ctot += cb;
+      if (vec) {
+        const size_t c0 = vidx.size();
+        vidx.resize(c0 + cb / 8, -1);
+        for (int32_t i = 0; i < cnt; ++i) vidx[c0 + i] = slot_row[s0 + i];
+      }
+      // then the wave's 16-byte mailbox packets (filled by the prober warp)
       sbytes[w] = (int32_t)(4 * (W.size() - base));
-      dbytes[w] = ((8 * NV * cnt + 15) & ~15) + 16 * (int32_t)pslot.size();
+      dbytes[w] = vb + cb + 16 * (int32_t)pslot.size();
       ssz[g].push_back(sbytes[w]);
       dsz[g].push_back(dbytes[w]);
     }
@@ -419,13 +462,13 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   // in-region dependencies through the mailbox, where the D-wave prefetch
   // finds them long published)
   auto fit = [&](int64_t SC, int32_t& D_, int32_t& cs_, int32_t& cd_) {
-    const int64_t fixed = 512 + 16 * (int64_t)R->max_waves + 8 * SC;
+    const int64_t fixed = 512 + 32 * (int64_t)R->max_waves + 8 * SC;
     const int64_t ring = (smem_budget - fixed) & ~(int64_t)15;
     if (ring < 1024) return false;
-    for (int D = 4; D >= 1; --D) {
+    for (int D = 8; D >= 1; --D) {
       const int32_t cd = min_cap(dsz, D, (int32_t)ring);
       if (cd < 0) continue;
-      const int32_t cs = min_cap(ssz, 2 * D, (int32_t)(ring - cd));
+      const int32_t cs = min_cap(ssz, D, (int32_t)(ring - cd));
       if (cs < 0) continue;
       D_ = D;
       cs_ = cs;
@@ -443,30 +486,34 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       bestD = D;
       bestSC = SC;
     }
-    if (bestD >= 3) break;
+    if (bestD >= 6) break;
   }
   if (bestD == 0) return -2;
   emit((int32_t)bestSC);
   {
     int32_t D = 0, cs = 0, cd = 0;
     fit(bestSC, D, cs, cd);
-    R->S = 2 * D;
+    R->S = D;
     R->D = D;
     R->CS = cs;
     R->CD = cd;
     R->SC = (int32_t)bestSC;
   }
-  R->table.assign((size_t)4 * nw, 0);
+  R->table.assign((size_t)8 * nw, 0);
   std::vector<int32_t> so, dof;
   for (int32_t gg = 0; gg < nreg; ++gg) {
     ring_place(ssz[gg], R->CS, R->S, so);
     ring_place(dsz[gg], R->CD, R->D, dof);
     for (int32_t k = 0; k < R->reg_wave[gg + 1] - R->reg_wave[gg]; ++k) {
       const int64_t w = R->reg_wave[gg] + k;
-      R->table[4 * w + 0] = goff[w];   // 16-byte units
-      R->table[4 * w + 1] = sbytes[w];
-      R->table[4 * w + 2] = so[k];
-      R->table[4 * w + 3] = dof[k];
+      R->table[8 * w + 0] = goff[w];   // 16-byte units
+      R->table[8 * w + 1] = sbytes[w];
+      R->table[8 * w + 2] = so[k];
+      R->table[8 * w + 3] = dof[k];
+      R->table[8 * w + 4] = voff[w];   // 16-byte units
+      R->table[8 * w + 5] = vbytes[w];
+      R->table[8 * w + 6] = coff[w];   // 16-byte units
+      R->table[8 * w + 7] = cbytes[w];
     }
   }
   sizes[0] = 4 * (int64_t)W.size();
@@ -479,6 +526,8 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   sizes[7] = R->CS;
   sizes[8] = R->CD;
   sizes[9] = R->ndeps_remote;
+  sizes[10] = (int64_t)R->sidx.size();
+  sizes[11] = (int64_t)R->vidx.size();
   std::lock_guard<std::mutex> lk(g_rs_mu);
   const int64_t h = g_rs_next++;
   g_rs[h] = std::move(R);
@@ -488,7 +537,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
 // Copy a built stream out (host buffers sized from jv_rstream_build's
 // sizes) and release it.
 extern "C" int jv_rstream_export(int64_t handle, int32_t* words, int32_t* table,
-                                 int32_t* reg_wave) {
+                                 int32_t* reg_wave, int32_t* sidx, int32_t* vidx) {
   std::unique_ptr<RStream> R;
   {
     std::lock_guard<std::mutex> lk(g_rs_mu);
@@ -500,5 +549,7 @@ extern "C" int jv_rstream_export(int64_t handle, int32_t* words, int32_t* table,
   std::memcpy(words, R->words.data(), 4 * R->words.size());
   std::memcpy(table, R->table.data(), 4 * R->table.size());
   std::memcpy(reg_wave, R->reg_wave.data(), 4 * R->reg_wave.size());
+  std::memcpy(sidx, R->sidx.data(), 4 * R->sidx.size());
+  std::memcpy(vidx, R->vidx.data(), 4 * R->vidx.size());
   return JV_OK;
 }

@@ -356,6 +356,7 @@ class DevIlu:
         self._rchoice = {}
         self.autotune_ms = {}
         self._hpat = None
+        self._vver = 0
         self._elim = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
@@ -554,6 +555,7 @@ class DevIlu:
             for rep in range(2):
                 if sweep == "factor":
                     self.val.copy_(save)
+                    self.values_changed()
                 ev[2 * rep].record()
                 fn()
                 ev[2 * rep + 1].record()
@@ -561,6 +563,7 @@ class DevIlu:
             times.append(ev[2].elapsed_time(ev[3]))
         if sweep == "factor":
             self.val.copy_(save)
+            self.values_changed()
             _lib.call("jv_reset_row", ptr(self.err), stream())
         check_hang()
         self.autotune_ms[sweep] = tuple(times)
@@ -604,10 +607,11 @@ class DevIlu:
         when the region path does not apply."""
         if not self.use_regions:
             return None
-        if sweep not in self._rstreams:
-            self._rstreams[sweep] = self._build_rstream(sweep) or False
+        key = (sweep, sweep == "factor" and self.tau > 0)
+        if key not in self._rstreams:
+            self._rstreams[key] = self._build_rstream(sweep) or False
             self._rchoice.pop(sweep, None)
-        return self._rstreams[sweep] or None
+        return self._rstreams[key] or None
 
     def _build_rstream(self, sweep):
         if self.n < self.region_min_rows:
@@ -626,14 +630,36 @@ class DevIlu:
         if ws is None:
             return None
         up = lambda a: t.from_numpy(np.ascontiguousarray(a)).to("cuda")
+        m, mv = int(ws.sidx.size), int(ws.vidx.size)
         return dict(nreg=nreg, words=up(ws.words), table=up(ws.table), reg_wave=up(ws.reg_wave),
+                    sidx=up(ws.sidx) if m else None, m=m,
+                    pack=t.empty(max(m, 2), dtype=t.float64, device="cuda"), pver=-1,
+                    vidx=up(ws.vidx) if mv else None, mv=mv,
+                    vpack=t.empty(max(mv, 2), dtype=t.float64, device="cuda"),
                     slot_ring=ws.slot_ring, max_waves=ws.max_waves, S=ws.S, D=ws.D, CS=ws.CS,
                     CD=ws.CD, waves=ws.waves, remote_deps=ws.remote_deps)
 
+    def values_changed(self):
+        """Invalidate the wave-ordered value copies (call after writing val)."""
+        self._vver += 1
+
+    def _pack(self, rp):
+        """Refresh the sweep's wave-ordered copy of the matrix values."""
+        if rp["pver"] != self._vver:
+            _lib.call("jv_pack_values", rp["m"], ptr(rp["sidx"]), ptr(self.val), ptr(rp["pack"]),
+                      stream())
+            rp["pver"] = self._vver
+
     def _region_run(self, rp, kind, inp, out, box):
+        self._pack(rp)
+        if rp["mv"]:
+            src = inp if kind != 0 else self.norms
+            _lib.call("jv_pack_values", rp["mv"], ptr(rp["vidx"]), ptr(src), ptr(rp["vpack"]),
+                      stream())
         _lib.call("jv_region_run", kind, rp["nreg"], ptr(rp["words"]), ptr(rp["table"]),
                   ptr(rp["reg_wave"]), rp["slot_ring"], rp["max_waves"], rp["S"], rp["D"],
-                  rp["CS"], rp["CD"], ptr(self.val), ptr(inp), ptr(out), ptr(self.norms),
+                  rp["CS"], rp["CD"], ptr(self.val), ptr(rp["pack"]), ptr(rp["vpack"]),
+                  ptr(out), ptr(self.norms),
                   self.tau, ptr(box.buf), box.next_epoch(), ptr(self.err), stream())
 
     def factor_async(self, lo=0, hi=None, ready_below=0, norms=True):
@@ -643,8 +669,10 @@ class DevIlu:
             rp = self._region_for("factor")
             if rp is not None:
                 self._factor_region(rp, norms)
+                self.values_changed()
                 return
         self._factor_tickets(lo, hi, ready_below, norms)
+        self.values_changed()
 
     def _factor_region(self, rp, norms):
         if norms and self.tau > 0:

@@ -35,6 +35,7 @@ class IluPlan:
 
     def reset_values(self):
         self.ilu.val.copy_(self.assembled)
+        self.ilu.values_changed()
 
 
 def _inverse(perm_d):

@@ -43,7 +43,10 @@ class WaveStream:
     kind: int
     nreg: int
     words: np.ndarray      # int32, 16-byte aligned wave blocks
-    table: np.ndarray      # int32 [waves, 4] {block offset (16 B), bytes, ring off, dyn off}
+    table: np.ndarray      # int32 [waves, 8] {block (16 B units), bytes, ring off, dyn off,
+                           #  packed values (16 B units), bytes, packed vector (16 B units), bytes}
+    sidx: np.ndarray       # int32 packed value -> position in val (-1: padding)
+    vidx: np.ndarray       # int32 packed per-call vector -> row (-1: padding)
     reg_wave: np.ndarray   # int32 [nreg + 1]
     slot_ring: int         # in-region values ring (power of 2)
     max_waves: int
@@ -66,22 +69,41 @@ def build_stream(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau=
                  threads=None):
     """WaveStream of one sweep ("factor", "fwd", "bwd"), or None when a row
     does not qualify (factor: not stencil-class; solves: > 32 dependencies)
-    or the plan does not fit in `smem_budget` bytes of shared memory."""
+    or the plan does not fit in `smem_budget` bytes of shared memory.
+    Without `threads`, waves of up to 512 rows are tried first and smaller
+    ones when the rings would only allow a short prefetch distance."""
+    if threads is None:
+        best = None
+        for t in (512, 256, 128):
+            ws = _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, t)
+            if ws is not None and (best is None or ws.D > best.D):
+                best = ws
+            if best is not None and best.D >= 6:
+                break
+        return best
+    return _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, threads)
+
+
+def _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, threads):
     lib = _lib.load()
     kind = KINDS[sweep]
     rs, cl, dg, ro = _i32(row_start), _i32(col), _i32(diag), _i32(region_of)
-    threads = lib.jv_region_threads() if threads is None else int(threads)
-    sizes = np.zeros(10, np.int64)
+    threads = min(int(threads), lib.jv_region_threads())
+    sizes = np.zeros(12, np.int64)
     h = lib.jv_rstream_build(kind, dg.size, _p(rs), _p(cl), _p(dg), _p(ro), int(nreg), threads,
                              int(smem_budget), int(tau > 0), _p(sizes))
     if h <= 0:
         return None
     words = np.empty(int(sizes[0]) // 4, np.int32)
-    table = np.empty((int(sizes[1]), 4), np.int32)
+    table = np.empty((int(sizes[1]), 8), np.int32)
     reg_wave = np.empty(int(nreg) + 1, np.int32)
-    _lib.call("jv_rstream_export", ctypes.c_int64(h), _p(words), _p(table), _p(reg_wave))
-    return WaveStream(kind, int(nreg), words, table, reg_wave, int(sizes[3]), int(sizes[4]),
-                      int(sizes[5]), int(sizes[6]), int(sizes[7]), int(sizes[8]), int(sizes[9]))
+    sidx = np.empty(max(int(sizes[10]), 1), np.int32)
+    vidx = np.empty(max(int(sizes[11]), 1), np.int32)
+    _lib.call("jv_rstream_export", ctypes.c_int64(h), _p(words), _p(table), _p(reg_wave), _p(sidx),
+              _p(vidx))
+    return WaveStream(kind, int(nreg), words, table, sidx[:int(sizes[10])], vidx[:int(sizes[11])],
+                      reg_wave, int(sizes[3]),
+                      int(sizes[4]), int(sizes[5]), int(sizes[6]), int(sizes[7]), int(sizes[8]), int(sizes[9]))
 
 
 def records(ws: WaveStream, w):

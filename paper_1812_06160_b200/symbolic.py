@@ -79,6 +79,7 @@ class IluFactors:
         d = self.device()
         if self.pattern.nnz:
             dv.upload_f64(d.val, self.val)
+        d.values_changed()
         return d
 
 

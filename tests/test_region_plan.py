@@ -74,11 +74,45 @@ def test_partition_acyclic_balanced(name):
     assert _quotient_is_acyclic(rs, col, diag, region_of, nreg)
 
 
+def _check_pack(ws, rs, diag, val):
+    """The packed copy (val[sidx]) holds, per wave, vals_m[k][i] in the
+    layout region.cu reads."""
+    packed = np.where(ws.sidx >= 0, val[np.maximum(ws.sidx, 0)], 0.0)
+    for w in range(ws.waves):
+        _, recs = RP.records(ws, w)
+        off = int(ws.table[w, 4]) * 2
+        K, cnt = recs[0]["K"], recs[0]["cnt"]
+        m = packed[off:off + int(ws.table[w, 5]) // 8]
+        for i, rc in enumerate(recs):
+            p0, nd = rc["p0"], rc["nd"]
+            if ws.kind == 0:
+                want = [(k, p0 + k) for k in range(nd)] + [(K, p0 + nd)] + \
+                       [(K + 1 + k, int(rc["us"][k])) for k in range(nd)]
+            elif ws.kind == 1:
+                want = [(k, p0 + k) for k in range(nd)]
+            else:
+                want = [(k, p0 + k) for k in range(nd + 1)]
+            for k, pos in want:
+                assert m[k * cnt + i] == val[pos]
+
+
+def _check_vec(ws):
+    """The packed per-call vector (x[vidx]) holds, per wave, x[row_i]."""
+    for w in range(ws.waves):
+        _, recs = RP.records(ws, w)
+        off = int(ws.table[w, 6]) * 2
+        for i, rc in enumerate(recs):
+            assert ws.vidx[off + i] == rc["r"]
+
+
 def _replay(ws, rs, col, diag, val, vec, tau=0.0, norms=None):
     """Execute the stream on the host: returns the output vector (solves)
     or the factored values (factor)."""
     n = diag.size
     kind = ws.kind
+    _check_pack(ws, rs, diag, val)
+    if ws.kind != 0:
+        _check_vec(ws)
     val = val.copy()
     out = np.full(n, np.nan)
     published = {}                      # mailbox slot -> value
@@ -153,10 +187,7 @@ def _ring_ok(ws):
                 if kind == "s":
                     size = int(ws.table[w, 1])
                 else:
-                    _, recs = RP.records(ws, w)
-                    K, cnt, NP = recs[0]["K"], recs[0]["cnt"], recs[0]["NP"]
-                    nv = {0: 2 * K + 1, 1: K + 1, 2: K + 2}[ws.kind]
-                    size = ((8 * nv * cnt + 15) & ~15) + 16 * NP
+                    size = int(ws.table[w, 5]) + int(ws.table[w, 7])
                 off = int(ws.table[w, col_off])
                 assert off % 16 == 0 and off + size <= cap
                 for (o2, s2) in blocks[-win:]:

@@ -73,7 +73,7 @@ for mode in ("tickets", "regions"):
                       "fwd_us": round(t_fwd, 1), "bwd_us": round(t_bwd, 1), "info": info}), flush=True)
 same = [bool(np.array_equal(res["tickets"][i], res["regions"][i])) for i in range(3)]
 from paper_1812_06160_b200 import _lib as _L
-for fl in (0, 4, 8, 12, 16, 28):
+for fl in (0, 4, 8, 12):
     _L.call("jv_set_region_flags", fl)
     print(json.dumps({"flags": fl, "factor_us": round(timed(lambda: (plan.reset_values(), ilu.factor_async())) - timed(lambda: plan.reset_values()), 1),
                       "fwd_us": round(timed(lambda: ilu.solve_async(0, b, y)), 1), "bwd_us": round(timed(lambda: ilu.solve_async(1, y, x)), 1)}), flush=True)
