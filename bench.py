@@ -353,7 +353,6 @@ def run_mine(args):
         if ev is not None:
             ev[4].record()
 
-    launches_per_step = 6   # norms, reset_row, factor, fwd, bwd, spmv
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -370,11 +369,15 @@ def run_mine(args):
     t1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
+    from paper_1812_06160_b200 import _lib as _L
+    _L.launch_counts.clear()
     torch.cuda.synchronize()
     t0.record()
     for k in range(args.steps):
         step(evs[k])
     t1.record()
+    launches = sum(_L.launch_counts.values())
+    launch_detail = dict(_L.launch_counts)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -420,7 +423,10 @@ def run_mine(args):
     # per-GPU algorithmic bytes (every rank factors its own matrix / shard)
     ach = ab["factor"] / f_avg / 1e9
     prof = load_profile(args.config)
+    impl = {sw: ("region" if ilu._region_for(sw) is not None else "tickets")
+            for sw in ("factor", "fwd", "bwd")}
     paths = {
+        "impl": impl, "autotune_ms": {k: list(v) for k, v in ilu.autotune_ms.items()},
         "factor": {"us": f_avg * 1e6, "nnz_per_s": nnz_f / f_avg, "alg_bytes": ab["factor"],
                    "GBps": ab["factor"] / f_avg / 1e9, "frac": ab["factor"] / f_avg / 1e9 / peak},
         "stri": {"us": st_avg * 1e6, "alg_bytes": ab["stri"], "GBps": ab["stri"] / st_avg / 1e9,
@@ -459,10 +465,11 @@ def run_mine(args):
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak, "peak_kind": peak_kind,
                      "traffic": prof.get("factor_dram_bytes") if prof else None,
-                     "kernel": "factor_kernel"},
+                     "kernel": "factor_kernel" if impl["factor"] == "tickets" else "region_kernel<0>"},
         "paths": paths,
         "e2e": e2e,
-        "gpu_launches": launches_per_step * K,
+        "gpu_launches": launches,
+        "gpu_launch_detail": launch_detail,
         "clocks": clocks,
         "parity_vs_reference": parity,
         "zero_pivot_row": bad,

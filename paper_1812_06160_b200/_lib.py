@@ -117,9 +117,18 @@ def exported_symbols():
     return list(_SIGS)
 
 
+# hot-path entry points that launch exactly one kernel of ours per call;
+# launch_counts tallies them (bench.py reports the count it observes)
+_ONE_LAUNCH = {"jv_factor", "jv_solve", "jv_region_run", "jv_pack_values", "jv_row_norms",
+               "jv_reset_row", "jv_spmv", "jv_spmv_rows", "jv_gather", "jv_check_zero_diag"}
+launch_counts = {}
+
+
 def call(name, *args):
     """Invoke a status-returning entry point; raise on a nonzero status."""
     lib = load()
+    if name in _ONE_LAUNCH:
+        launch_counts[name] = launch_counts.get(name, 0) + 1
     rc = getattr(lib, name)(*args)
     if rc != 0:
         msg = lib.jv_last_error().decode(errors="replace")

@@ -178,17 +178,21 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
     unsigned ns = 0, spins = 0;
     while (lo < nw) {
       // admit waves whose blocks are in (non-blocking)
+      // (its packets are copied unconditionally: the area holds stale data)
+      bool issued = false;
+      const int hi0 = hi;
       while (hi < nw && hi < lo + kWin && bar_test(&bar[hi % kNB], (uint32_t)((hi / kNB) & 1))) {
         const Wave X(sring + tab[2 * hi].z);
         unsigned char* pk = pkts(hi);
-        for (int j = lane; j < X.NP; j += 32)
-          *reinterpret_cast<ulonglong2*>(pk + 16 * j) = make_ulonglong2(0ull, 0ull);
+        if (!(flags & 8))
+          for (int j = lane; j < X.NP; j += 32) {
+            cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot<KIND>(j));
+            issued = true;
+          }
         ++hi;
       }
-      __syncwarp();
       // one round: copy every stale packet of the window
-      bool issued = false;
-      for (int x = lo; x < hi; ++x) {
+      for (int x = lo; x < hi0; ++x) {
         const Wave X(sring + tab[2 * x].z);
         unsigned char* pk = pkts(x);
         for (int j = lane; j < X.NP; j += 32)

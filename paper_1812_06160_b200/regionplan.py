@@ -71,14 +71,16 @@ def build_stream(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau=
     does not qualify (factor: not stencil-class; solves: > 32 dependencies)
     or the plan does not fit in `smem_budget` bytes of shared memory.
     Without `threads`, waves of up to 512 rows are tried first and smaller
-    ones when the rings would only allow a short prefetch distance."""
+    ones when the rings would only allow a prefetch distance below 3."""
     if threads is None:
+        # wider waves mean fewer barrier steps on the critical path: take the
+        # widest that still prefetches >= 3 waves ahead
         best = None
         for t in (512, 256, 128):
             ws = _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, t)
             if ws is not None and (best is None or ws.D > best.D):
                 best = ws
-            if best is not None and best.D >= 6:
+            if best is not None and best.D >= 3:
                 break
         return best
     return _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, threads)
