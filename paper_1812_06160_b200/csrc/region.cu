@@ -94,9 +94,8 @@ struct Wave {
   JV_INLINE int p0(int i) const { return b[4 + cnt + i]; }
   JV_INLINE int meta(int i) const { return b[4 + 2 * cnt + i]; }
   JV_INLINE int ref(int k, int i) const { return b[4 + (3 + k) * cnt + i]; }
-  JV_INLINE int us(int k, int i) const { return b[4 + (3 + K + k) * cnt + i]; }
   template <int KIND>
-  JV_INLINE int pslot(int j) const { return b[4 + (3 + (KIND == 0 ? 2 * K : K)) * cnt + j]; }
+  JV_INLINE int pslot(int j) const { return b[4 + (3 + K) * cnt + j]; }
 };
 constexpr int kCompute = 512;
 constexpr int kBlock = kCompute + 64;   // + a producer warp (one lane) and a prober warp

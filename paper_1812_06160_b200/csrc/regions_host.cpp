@@ -20,11 +20,11 @@
 //    slots; consecutive rows of one level in waves of <= threads rows; every
 //    wave is a 16-byte aligned structure-of-arrays block of int32 words
 //        [cnt, slot0, K, NP, row[cnt], p0[cnt], meta[cnt], ref[K][cnt],
-//         (factor) us[K][cnt], pslot[NP]]
+//         pslot[NP]]
 //    K = most dependencies of a row in the wave, meta = ndep | pub << 6 |
 //    umask << 7 (factor), ref >= 0: slot in the region's ring, < 0:
 //    -(1 + j), the wave's j-th remote dependency, mailbox slot pslot[j];
-//    us = positions of u(c_k, r) (factor).  The wave's dynamic block holds
+//    The factor's u(c_k, r) come with the packed values.  The wave's dynamic block holds
 //    vals[NV][cnt] (matrix values, right-hand side; gathered at run time)
 //    and NP 16-byte mailbox packets.  Static blocks are bulk-copied (TMA) S waves ahead into
 //    a shared-memory ring, dynamic blocks gathered D waves ahead; ring
@@ -373,7 +373,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
         const int32_t r = slot_row[s0 + i];
         K = std::max(K, dep_hi(r) - dep_lo(r));
       }
-      // SoA block: header, r[], p0[], meta[], ref[K][], (factor) us[K][], pslot[]
+      // SoA block: header, r[], p0[], meta[], ref[K][], pslot[]
       ref.assign((size_t)K * cnt, 0);
       pslot.clear();
       const size_t base = W.size();
@@ -407,10 +407,6 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       W[base + 2] = K;
       W[base + 3] = (int32_t)pslot.size();
       W.insert(W.end(), ref.begin(), ref.end());
-      if (kind == 0) {
-        for (int32_t k = 0; k < K; ++k)
-          for (int32_t i = 0; i < cnt; ++i) W.push_back(us[(size_t)4 * slot_row[s0 + i] + k]);
-      }
       W.insert(W.end(), pslot.begin(), pslot.end());
       while ((W.size() - base) % 4) W.push_back(0);
       // values of the wave, packed once per factorization into a global

@@ -116,10 +116,6 @@ def records(ws: WaveStream, w):
     row, p0, meta = blk[4:4 + cnt], blk[4 + cnt:4 + 2 * cnt], blk[4 + 2 * cnt:4 + 3 * cnt]
     ref = blk[4 + 3 * cnt:4 + (3 + K) * cnt].reshape(K, cnt)
     off = 4 + (3 + K) * cnt
-    us = None
-    if ws.kind == 0:
-        us = blk[off:off + K * cnt].reshape(K, cnt)
-        off += K * cnt
     pslot = blk[off:off + NP]
     out = []
     for i in range(cnt):
@@ -128,5 +124,5 @@ def records(ws: WaveStream, w):
         out.append(dict(r=int(row[i]), p0=int(p0[i]), nd=nd, pub=(int(meta[i]) >> 6) & 1,
                         umask=(int(meta[i]) >> 7) & 15, refs=refs,
                         rsl=np.array([pslot[-1 - int(x)] for x in refs if x < 0], np.int64),
-                        us=None if us is None else us[:nd, i], K=K, cnt=cnt, NP=NP))
+                        K=K, cnt=cnt, NP=NP))
     return slot0, out

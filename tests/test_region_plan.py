@@ -74,7 +74,15 @@ def test_partition_acyclic_balanced(name):
     assert _quotient_is_acyclic(rs, col, diag, region_of, nreg)
 
 
-def _check_pack(ws, rs, diag, val):
+def _upos(rs, col, diag, r, k):
+    """position of u(c_k, r) in val: row c_k's upper entry in column r (-1: none)"""
+    c = int(col[rs[r] + k])
+    seg = col[diag[c] + 1:rs[c + 1]]
+    hit = np.nonzero(seg == r)[0]
+    return int(diag[c] + 1 + hit[0]) if hit.size else -1
+
+
+def _check_pack(ws, rs, diag, val, col=None):
     """The packed copy (val[sidx]) holds, per wave, vals_m[k][i] in the
     layout region.cu reads."""
     packed = np.where(ws.sidx >= 0, val[np.maximum(ws.sidx, 0)], 0.0)
@@ -87,7 +95,8 @@ def _check_pack(ws, rs, diag, val):
             p0, nd = rc["p0"], rc["nd"]
             if ws.kind == 0:
                 want = [(k, p0 + k) for k in range(nd)] + [(K, p0 + nd)] + \
-                       [(K + 1 + k, int(rc["us"][k])) for k in range(nd)]
+                       [(K + 1 + k, _upos(rs, col, diag, rc["r"], k)) for k in range(nd)
+                        if _upos(rs, col, diag, rc["r"], k) >= 0]
             elif ws.kind == 1:
                 want = [(k, p0 + k) for k in range(nd)]
             else:
@@ -110,7 +119,7 @@ def _replay(ws, rs, col, diag, val, vec, tau=0.0, norms=None):
     or the factored values (factor)."""
     n = diag.size
     kind = ws.kind
-    _check_pack(ws, rs, diag, val)
+    _check_pack(ws, rs, diag, val, col)
     if ws.kind != 0:
         _check_vec(ws)
     val = val.copy()
@@ -149,7 +158,7 @@ def _replay(ws, rs, col, diag, val, vec, tau=0.0, norms=None):
                             if tau > 0 and abs(l) < thresh:
                                 l = 0.0
                             elif rc["umask"] >> kk & 1:
-                                d = d - l * val[int(rc["us"][kk])]
+                                d = d - l * val[_upos(rs, col, diag, r, kk)]
                             val[p0 + kk] = l
                         val[p0 + nd] = d
                         x, key = d, p0 + nd
