@@ -83,6 +83,13 @@ def main():
         "level_hop_us_median": float(np.median(hop)) / 1e3 if hop.size else None,
         "warp_class_batches": int((cls == 1).sum()),
     }
+    # time per level: where the makespan goes
+    lev_start = np.array([t[lev == L, 0].min() for L in range(nlev)])
+    sizes = np.bincount(lev, minlength=nlev)
+    span = lev_end - np.concatenate([[0], lev_end[:-1]])
+    top = np.argsort(-span)[:8]
+    out["top_levels(level,batches,us_added)"] = [(int(L), int(sizes[L]), float(span[L]) / 1e3) for L in top]
+    out["busy_warps_frac_by_quartile"] = [float(x) for x in np.percentile(span, [25, 50, 75, 100]) / 1e3]
     print(json.dumps(out))
 
 
