@@ -99,7 +99,7 @@ struct Wave {
 };
 constexpr int kCompute = 512;
 constexpr int kBlock = kCompute + 64;   // + a producer warp (one lane) and a prober warp
-constexpr int kWin = 8;                 // prober window (waves)
+constexpr int kWin = 16;                // prober window (waves)
 
 JV_INLINE void cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(dst)), "l"(src) : "memory");
@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
   const int tid = threadIdx.x;
   uint64_t* bar = reinterpret_cast<uint64_t*>(rsm);            // wave full [kNB]
   int* done = reinterpret_cast<int*>(rsm + 8 * kNB);          // waves finished
-  int* probed = done + 1;                                       // waves whose remote deps are in
+  int* probed = done + 1;   // waves below are released by the prober
+  int* issued = done + 2;   // waves whose blocks the producer has issued
   int4* tab = reinterpret_cast<int4*>(rsm + 256);             // 2 per wave
   double* slot = reinterpret_cast<double*>(rsm + 256 + 32 * A.max_waves);
   unsigned char* sring = rsm + 256 + 32 * A.max_waves + 8 * A.SC;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
     for (int b = 0; b < kNB; ++b) bar_init(&bar[b], 1);
     *done = 0;
     *probed = 0;
+    *issued = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -167,8 +169,9 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
     const int lane = tid - kCompute - 32;
     auto pkts = [&](int x) -> unsigned char* {
       const int4 v = tab[2 * x + 1];
-      return dring + tab[2 * x].w + v.y + v.w;
+      return dring + tab[2 * x].w + v.y + (v.w & 0xffff);
     };
+    auto np = [&](int x) { return tab[2 * x + 1].w >> 16; };
     auto fresh = [&](const unsigned char* p) {
       const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(p);
       return (uint32_t)(q.x >> 32) == A.epoch && (uint32_t)(q.y >> 32) == A.epoch;
@@ -176,40 +179,49 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
     int lo = 0, hi = 0;
     unsigned ns = 0, spins = 0;
     while (lo < nw) {
-      // admit waves whose blocks are in (non-blocking)
-      // (its packets are copied unconditionally: the area holds stale data)
-      bool issued = false;
+      // admit waves: one without remote dependencies needs nothing; one with
+      // them once the producer has issued it and its blocks are in (its
+      // packets are then copied unconditionally: the area holds stale data)
+      bool issued_any = false;
       const int hi0 = hi;
-      while (hi < nw && hi < lo + kWin && bar_test(&bar[hi % kNB], (uint32_t)((hi / kNB) & 1))) {
-        const Wave X(sring + tab[2 * hi].z);
-        unsigned char* pk = pkts(hi);
-        if (!(flags & 8))
-          for (int j = lane; j < X.NP; j += 32) {
-            cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot<KIND>(j));
-            issued = true;
-          }
+      const int iss = ld_volatile_shared(issued);
+      while (hi < nw && hi < lo + kWin) {
+        if (np(hi) > 0) {
+          if (hi >= iss || !bar_test(&bar[hi % kNB], (uint32_t)((hi / kNB) & 1))) break;
+          const Wave X(sring + tab[2 * hi].z);
+          unsigned char* pk = pkts(hi);
+          if (!(flags & 8))
+            for (int j = lane; j < X.NP; j += 32) {
+              cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot<KIND>(j));
+              issued_any = true;
+            }
+        }
         ++hi;
       }
       // one round: copy every stale packet of the window
       for (int x = lo; x < hi0; ++x) {
+        if (np(x) == 0) continue;
         const Wave X(sring + tab[2 * x].z);
         unsigned char* pk = pkts(x);
         for (int j = lane; j < X.NP; j += 32)
           if (!fresh(pk + 16 * j) && !(flags & 8)) {
             cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot<KIND>(j));
-            issued = true;
+            issued_any = true;
           }
       }
-      asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+      if (__any_sync(full, issued_any))
+        asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
       // release the leading waves that are complete
       const int lo0 = lo;
       while (lo < hi) {
-        const Wave X(sring + tab[2 * lo].z);
-        const unsigned char* pk = pkts(lo);
-        bool ok = true;
-        for (int j = lane; j < X.NP; j += 32) ok = ok && ((flags & 8) || fresh(pk + 16 * j));
-        if (!__all_sync(full, ok)) break;
+        if (np(lo) > 0) {
+          const Wave X(sring + tab[2 * lo].z);
+          const unsigned char* pk = pkts(lo);
+          bool ok = true;
+          for (int j = lane; j < X.NP; j += 32) ok = ok && ((flags & 8) || fresh(pk + 16 * j));
+          if (!__all_sync(full, ok)) break;
+        }
         ++lo;
       }
       if (lo != lo0) {
@@ -219,7 +231,7 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
         }
         ns = 0;
         spins = 0;
-      } else if (!__any_sync(full, issued) || hi == lo) {
+      } else if (!__any_sync(full, issued_any)) {
         // nothing in flight: wait for the producer (or a slow upstream)
         if (ns) __nanosleep(ns);
         ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
       const int4 t2 = tab[2 * x], v2 = tab[2 * x + 1];
       l2_prefetch_bulk(A.words + t2.x, (uint32_t)t2.y);
       if (v2.y > 0) l2_prefetch_bulk(A.pack + 2 * (int64_t)v2.x, (uint32_t)v2.y);
-      if (v2.w > 0) l2_prefetch_bulk(A.vpack + 2 * (int64_t)v2.z, (uint32_t)v2.w);
+      if (v2.w & 0xffff) l2_prefetch_bulk(A.vpack + 2 * (int64_t)v2.z, (uint32_t)(v2.w & 0xffff));
     };
     for (int x = 0; x < kL2 && x < nw; ++x) prefetch(x);
     for (int x = 0; x < nw; ++x) {
@@ -251,11 +263,13 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
       const int4 t = tab[2 * x], v = tab[2 * x + 1];
       uint64_t* b = &bar[x % kNB];
       const bool skip = flags & 4;   // diagnostic: no value copies (wrong results)
-      bar_expect_tx(b, (uint32_t)(t.y + (skip ? 0 : v.y + v.w)));
+      const int cb = v.w & 0xffff;
+      bar_expect_tx(b, (uint32_t)(t.y + (skip ? 0 : v.y + cb)));
       bulk_g2s(sring + t.z, A.words + t.x, (uint32_t)t.y, b);
       unsigned char* blk = dring + t.w;
       if (!skip && v.y > 0) bulk_g2s(blk, A.pack + 2 * (int64_t)v.x, (uint32_t)v.y, b);
-      if (!skip && v.w > 0) bulk_g2s(blk + v.y, A.vpack + 2 * (int64_t)v.z, (uint32_t)v.w, b);
+      if (!skip && cb > 0) bulk_g2s(blk + v.y, A.vpack + 2 * (int64_t)v.z, (uint32_t)cb, b);
+      asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(issued)), "r"(x + 1) : "memory");
     }
     return;
   }
@@ -273,18 +287,21 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
     const bool active = tid < cnt;
     const double* vals = reinterpret_cast<const double*>(dring + t.w);
     const double* vec = reinterpret_cast<const double*>(dring + t.w + tv.y);
-    const unsigned char* pk = dring + t.w + tv.y + tv.w;
+    const unsigned char* pk = dring + t.w + tv.y + (tv.w & 0xffff);
     auto val = [&](int k) -> double { return vals[k * cnt + tid]; };
     auto packet = [&](int j) -> double {
       const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(pk + 16 * j);
       return __longlong_as_double((long long)((p.x & 0xffffffffull) | (p.y << 32)));
     };
     if (tid == 0) jv::trace_mark(T, w0 + w, 2);
-    // the prober has this wave's remote dependencies (every wave passes
-    // through the prober, so it never looks at a ring block already reused)
-    while (ld_volatile_shared(probed) <= w) {
+    // the prober has released this wave's remote dependencies (a wave
+    // without any passes straight through; the prober never reads its ring
+    // blocks, so their reuse needs no handshake)
+    if ((tv.w >> 16) > 0) {
+      while (ld_volatile_shared(probed) <= w) {
+      }
+      __threadfence_block();
     }
-    __threadfence_block();
     double dv[kR];
     int nd = 0, meta = 0;
     if (active) {

@@ -342,7 +342,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   std::vector<int32_t> goff(nw), sbytes(nw), dbytes(nw), voff(nw), vbytes(nw);
   std::vector<int32_t>& sidx = R->sidx;
   std::vector<int32_t>& vidx = R->vidx;
-  std::vector<int32_t> coff(nw), cbytes(nw);
+  std::vector<int32_t> coff(nw), cbytes(nw), npk(nw);
   int64_t vtot = 0, ctot = 0;
   std::vector<std::vector<int32_t>> ssz(nreg), dsz(nreg);
   std::vector<int32_t>& W = R->words;
@@ -449,6 +449,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       // then the wave's 16-byte mailbox packets (filled by the prober warp)
       sbytes[w] = (int32_t)(4 * (W.size() - base));
       dbytes[w] = vb + cb + 16 * (int32_t)pslot.size();
+      npk[w] = (int32_t)pslot.size();
       ssz[g].push_back(sbytes[w]);
       dsz[g].push_back(dbytes[w]);
     }
@@ -509,7 +510,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       R->table[8 * w + 4] = voff[w];   // 16-byte units
       R->table[8 * w + 5] = vbytes[w];
       R->table[8 * w + 6] = coff[w];   // 16-byte units
-      R->table[8 * w + 7] = cbytes[w];
+      R->table[8 * w + 7] = cbytes[w] | (npk[w] << 16);   // | remote packets of the wave
     }
   }
   sizes[0] = 4 * (int64_t)W.size();

@@ -569,6 +569,7 @@ class DevIlu:
         self.autotune_ms[sweep] = tuple(times)
         return times[1] < times[0]
     region_min_rows = 64
+    region_single_max = 32768   # rows: up to here one region (one CTA) holds the matrix
     region_hint = None
     KIND = {"factor": 0, "fwd": 1, "bwd": 2}
 
@@ -600,7 +601,9 @@ class DevIlu:
         rs, col, diag = self._host_pattern()
         t = torch()
         sms = t.cuda.get_device_properties(t.cuda.current_device()).multi_processor_count
-        return regionplan.partition(rs, col, diag, sms)
+        # a small matrix fits one CTA: no cross-region hops at all
+        nreg = 1 if self.n <= self.region_single_max else sms
+        return regionplan.partition(rs, col, diag, nreg)
 
     def region_stream(self, sweep):
         """Device wave stream of one sweep ("factor", "fwd", "bwd") or None

@@ -36,15 +36,20 @@ def _front(a, k, tau):
 
 
 @pytest.mark.parametrize("name", NAMES)
-@pytest.mark.parametrize("mode", ["on", "off", "auto"])
+@pytest.mark.parametrize("mode", ["on", "on-single", "off", "auto"])
 def test_region_paths_bitwise(name, mode):
+    """on: one region per SM (cross-region mailboxes); on-single: the whole
+    matrix in one CTA; off: ticket kernels; auto: the faster per sweep."""
     a, k, tau = _case(name)
     rs, col, diag, val = _front(a, k, tau)
     n = diag.size
     want, bad = oracle.factor_serial(rs, col, val.copy(), diag, tau, False)
     assert bad < 0
     d = dv.DevIlu.from_host(n, rs, col, diag, val, tau=tau)
-    d.region_mode = mode
+    d.region_single_max = n if mode == "on-single" else 0
+    d.region_mode = "on" if mode.startswith("on") else mode
+    if mode == "on-single":
+        assert d.regions()[0] == 1
     if mode == "on":
         assert d.region_stream("fwd") is not None and d.region_stream("bwd") is not None
         stencil = name.startswith(("poisson", "laplace"))
@@ -78,6 +83,7 @@ def test_region_factor_zero_pivot_smallest_row():
     want, bad = oracle.factor_serial(rs, col, val.copy(), diag, 0.0, False)
     assert bad == 900
     d = dv.DevIlu.from_host(n, rs, col, diag, val)
+    d.region_single_max = 0
     d.region_mode = "on"
     assert d.region_stream("factor") is not None
     assert d.factor() == 900
@@ -93,6 +99,7 @@ def test_region_many_epochs():
     n = diag.size
     want, _ = oracle.factor_serial(rs, col, val.copy(), diag, 0.0, False)
     d = dv.DevIlu.from_host(n, rs, col, diag, val)
+    d.region_single_max = 0
     d.region_mode = "on"
     for _ in range(20):
         dv.upload_f64(d.val, val)
