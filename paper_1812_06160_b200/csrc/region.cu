@@ -307,13 +307,27 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
     if (active) {
       meta = V.meta(tid);
       nd = meta & 63;
+      // branch-free: every ref load, then both candidate values of every
+      // dependency (slot ring and packet; both addresses are in shared
+      // memory), then selects -- two load latencies instead of a chain
+      int ref[kR];
+#pragma unroll
+      for (int k = 0; k < kR; ++k) ref[k] = k < nd ? V.ref(k, tid) : 0;
+      double sv[kR];
+      ulonglong2 pv[kR];
 #pragma unroll
       for (int k = 0; k < kR; ++k) {
-        dv[k] = 1.0;
-        if (k < nd) {
-          const int ref = V.ref(k, tid);
-          dv[k] = ref >= 0 ? slot[ref] : packet(-1 - ref);
-        }
+        sv[k] = slot[max(ref[k], 0)];
+        // (a wave without packets may end at the ring's end: read the
+        // slot ring instead, the value is discarded)
+        pv[k] = *reinterpret_cast<const ulonglong2*>(
+            V.NP > 0 ? pk + 16 * max(-1 - ref[k], 0) : reinterpret_cast<const unsigned char*>(slot));
+      }
+#pragma unroll
+      for (int k = 0; k < kR; ++k) {
+        const double p = __longlong_as_double(
+            (long long)((pv[k].x & 0xffffffffull) | (pv[k].y << 32)));
+        dv[k] = k < nd ? (ref[k] >= 0 ? sv[k] : p) : 1.0;
       }
     }
     if (tid == 0) jv::trace_mark(T, w0 + w, 3);
