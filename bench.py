@@ -399,6 +399,28 @@ def run_mine(args):
     f_avg, st_avg, sp_avg = f_sum / K / 1e3, st_sum / K / 1e3, sp_sum / K / 1e3   # seconds
 
     parity = parity_check(args.config, ilu, plan, x, sy, blocks, n)
+
+    # the paper's CSR-LS baseline on this GPU (one launch per level, CUDA
+    # graph), for comparison with the sync-free / region sweeps; same bits
+    csrls = None
+    if not batched:
+        cy, cx = dv.empty_f64(n), dv.empty_f64(n)
+        ilu.solve_csrls_async(0, b, cy)
+        ilu.solve_csrls_async(1, cy, cx)
+        ce = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        cf, cb = [], []
+        for _ in range(5):
+            ce[0].record()
+            ilu.solve_csrls_async(0, b, cy)
+            ce[1].record()
+            ilu.solve_csrls_async(1, cy, cx)
+            ce[2].record()
+            torch.cuda.synchronize()
+            cf.append(ce[0].elapsed_time(ce[1]) * 1e3)
+            cb.append(ce[1].elapsed_time(ce[2]) * 1e3)
+        csrls = {"fwd_us": statistics.median(cf), "bwd_us": statistics.median(cb),
+                 "launches_per_sweep": ilu._csrls[0][3],
+                 "bitwise_equal_to_step": bool(torch.equal(cx, x))}
     if world > 1:
         pl = [None] * world
         dist.all_gather_object(pl, parity)
@@ -432,6 +454,7 @@ def run_mine(args):
         "stri": {"us": st_avg * 1e6, "alg_bytes": ab["stri"], "GBps": ab["stri"] / st_avg / 1e9,
                  "frac": ab["stri"] / st_avg / 1e9 / peak,
                  "fwd_us": sum(fw_ms) / K * 1e3, "bwd_us": sum(bw_ms) / K * 1e3},
+        "stri_csrls_baseline": csrls,
         "spmv": {"us": sp_avg * 1e6, "alg_bytes": ab["spmv"], "GBps": ab["spmv"] / sp_avg / 1e9,
                  "frac": ab["spmv"] / sp_avg / 1e9 / peak},
     }

@@ -238,6 +238,12 @@ int jv_solve(int which, int32_t n, const int32_t* row_start, const int32_t* col,
 /* ready_below analogue for solves is not needed: every solve path of the
  * reference (serial, csrls, ls, ls_lower; trisolve.py:60-182) produces the
  * same bits, so one sync-free sweep serves all of them. */
+/* one level of the paper's CSR-LS baseline stri (trisolve.py:74-108):
+ * rows order[lo:hi] of one level, thread per row, reference order; the host
+ * launches the levels back to back (a CUDA graph) */
+int jv_solve_level(int which, const int32_t* row_start, const int32_t* col, const double* val,
+                   const int32_t* diag_pos, const int32_t* order, int32_t lo, int32_t hi,
+                   const double* in, double* out, void* stream);
 int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,
                        int32_t* row, void* stream);
 /* schedule builder: cut every level of a level_sort result into batches of

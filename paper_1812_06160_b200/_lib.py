@@ -60,6 +60,7 @@ _SIGS = {
     "jv_elim_lists": [c_int32, _P, _P, _P, c_int, c_int64, _P, _P, _P, _P, POINTER(c_int64), _P],
     "jv_solve": [c_int, c_int32, _P, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, c_uint32, _P, _P],
     "jv_check_zero_diag": [c_int32, _P, _P, _P, _P],
+    "jv_solve_level": [c_int, _P, _P, _P, _P, _P, c_int32, c_int32, _P, _P, _P],
     "jv_build_batches": [c_int32, _P, _P, _I32P, _P],
     "jv_build_schedule": [c_int32, _P, _P, c_int32, _P, _P, _I32P, _P],
     "jv_hub_plan_host": [c_int32, c_int32, _P, _P, _P, _P, _P, POINTER(c_int64), _P,
@@ -120,7 +121,8 @@ def exported_symbols():
 # hot-path entry points that launch exactly one kernel of ours per call;
 # launch_counts tallies them (bench.py reports the count it observes)
 _ONE_LAUNCH = {"jv_factor", "jv_solve", "jv_region_run", "jv_pack_values", "jv_row_norms",
-               "jv_reset_row", "jv_spmv", "jv_spmv_rows", "jv_gather", "jv_check_zero_diag"}
+               "jv_reset_row", "jv_spmv", "jv_spmv_rows", "jv_gather", "jv_check_zero_diag",
+               "jv_solve_level"}
 launch_counts = {}
 
 

@@ -283,6 +283,30 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs A) {
   jv::ticket_exit(A.ticket, lane, W);
 }
 
+// One level of the paper's CSR-LS baseline (trisolve.py:74-108,
+// _kernels.py:369-401): thread per row of the level, the row's chain in the
+// reference order; the levels run as consecutive launches (captured into a
+// CUDA graph by the host), the launch boundary standing in for the
+// reference's barrier.
+__global__ void __launch_bounds__(256) level_solve_kernel(int which, const int32_t* rs,
+                                                          const int32_t* col, const double* val,
+                                                          const int32_t* diag,
+                                                          const int32_t* order, int lo, int hi,
+                                                          const double* in, double* out) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
+  const int r = order[i];
+  double s = in[r];
+  if (which == 0) {
+    for (int p = rs[r]; p < diag[r]; ++p) s = jv::dsub(s, jv::dmul(val[p], out[col[p]]));
+  } else {
+    const int d = diag[r];
+    for (int p = d + 1; p < rs[r + 1]; ++p) s = jv::dsub(s, jv::dmul(val[p], out[col[p]]));
+    s = jv::ddiv(s, val[d]);
+  }
+  out[r] = s;
+}
+
 __global__ void check_zero_diag_kernel(int n, const double* val, const int32_t* diag, int32_t* row) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     if (val[diag[r]] == 0.0) atomicMin(row, r);
@@ -315,6 +339,16 @@ extern "C" int jv_solve(int which, int32_t n, const int32_t* row_start, const in
                                   8 * kSolveStageBytes);
   return jvh::persistent_launch(solve_kernel<true>, 256, args, (cudaStream_t)stream, "jv_solve bwd",
                                 8 * kSolveStageBytes);
+}
+
+extern "C" int jv_solve_level(int which, const int32_t* row_start, const int32_t* col,
+                              const double* val, const int32_t* diag_pos, const int32_t* order,
+                              int32_t lo, int32_t hi, const double* in, double* out, void* stream) {
+  if (hi <= lo) return JV_OK;
+  level_solve_kernel<<<(hi - lo + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      which, row_start, col, val, diag_pos, order, lo, hi, in, out);
+  JV_CHECK_LAUNCH("jv_solve_level");
+  return JV_OK;
 }
 
 extern "C" int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,

@@ -357,6 +357,7 @@ class DevIlu:
         self.autotune_ms = {}
         self._hpat = None
         self._vver = 0
+        self._csrls = {}
         self._elim = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
@@ -728,6 +729,48 @@ class DevIlu:
                   ptr(self.diag_pos), ptr(sched.order), ptr(sched.batch_ptr), sched.nbatch,
                   ptr(b), ptr(out), ptr(self.sbox.buf), self.sbox.next_epoch(),
                   ctypes.c_void_p(self.ticket.data_ptr() + 8), stream())
+
+    # the paper's CSR-LS baseline on the GPU ----------------------------
+    def _csrls_graph(self, which):
+        """CUDA graph of one level-synchronous sweep (one launch per level)
+        over fixed in/out buffers; built once per pattern and direction."""
+        if which in self._csrls:
+            return self._csrls[which]
+        t = torch()
+        sched = self.fwd_schedule() if which == 0 else self.bwd_schedule()
+        nclass = len(sched.steps) if hasattr(sched, "steps") else 2
+        order = sched.order
+        keys = sched.keys[order.long()] // nclass
+        lev = keys.cpu().numpy()
+        nlev = int(lev.max()) + 1 if lev.size else 0
+        ptr_ = np.searchsorted(lev, np.arange(nlev + 1))
+        bin_ = t.zeros(self.n, dtype=t.float64, device="cuda")
+        bout = t.zeros(self.n, dtype=t.float64, device="cuda")
+        args = (ptr(self.row_start), ptr(self.col), ptr(self.val), ptr(self.diag_pos), ptr(order))
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):   # warm-up outside capture
+            for L in range(nlev):
+                _lib.load().jv_solve_level(which, *args, int(ptr_[L]), int(ptr_[L + 1]), ptr(bin_),
+                                           ptr(bout), stream())
+        t.cuda.current_stream().wait_stream(s)
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g):
+            for L in range(nlev):
+                _lib.load().jv_solve_level(which, *args, int(ptr_[L]), int(ptr_[L + 1]), ptr(bin_),
+                                           ptr(bout), stream())
+        self._csrls[which] = (g, bin_, bout, nlev)
+        return self._csrls[which]
+
+    def solve_csrls_async(self, which, b, out):
+        """Level-synchronous sweep (the paper's CSR-LS baseline): bitwise the
+        same result as solve_async."""
+        g, bin_, bout, nlev = self._csrls_graph(which)
+        bin_.copy_(b[:self.n])
+        g.replay()
+        _lib.launch_counts["jv_solve_level"] = _lib.launch_counts.get("jv_solve_level", 0) + nlev
+        out[:self.n].copy_(bout)
+        return out
 
     def host_val(self):
         return host_f64(self.val, self.nnz)

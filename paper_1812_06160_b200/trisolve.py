@@ -73,11 +73,24 @@ def solve_baseline_csrls(
     nthreads: int,
     which: str,
 ) -> np.ndarray:
-    """The paper's CSR-LS baseline entry point (trisolve.py:74-108)."""
+    """The paper's CSR-LS baseline (trisolve.py:74-108): one level at a time,
+    here one kernel launch per level replayed from a CUDA graph
+    (jv_solve_level) — the GPU counterpart of the reference's barrier per
+    level, kept for comparison with the sync-free and region sweeps."""
     _check_which(which)
     if schedule.n != factors.n:
         raise ConfigurationError("level schedule does not match the factors")
-    return _device_sweep(factors, b, which)
+    b = np.array(b, dtype=np.float64, copy=True)
+    if factors.n == 0:
+        return b
+    d = factors.upload_values()
+    if which == BACKWARD:
+        bad = d.first_zero_diag()
+        if bad >= 0:
+            raise ZeroPivotError(bad)
+    x = dv.f64(b)
+    d.solve_csrls_async(0 if which == FORWARD else 1, x, x)
+    return dv.host_f64(x, factors.n)
 
 
 def solve_ls(

@@ -106,3 +106,28 @@ def test_region_many_epochs():
         assert d.factor() == -1
     assert np.array_equal(d.host_val(), want)
     dv.check_hang()
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_csrls_baseline_bitwise(k):
+    """The paper's CSR-LS baseline (one launch per level, CUDA graph) gives
+    the reference's bits, like every other solve path."""
+    from paper_1812_06160_b200.ordering import LOWER_A_PLUS_AT
+    from paper_1812_06160_b200.trisolve import BACKWARD, FORWARD
+    a = W.convdiff3d(8, 2) if k else W.laplace7(12, 4)
+    src = jv.lower_pattern(jv.symmetrize_pattern(a.pattern))
+    sched = jv.compute_levels(src, LOWER_A_PLUS_AT)
+    part = jv.partition_stages(sched, np.diff(a.row_start))
+    perm = jv.build_level_permutation(part)
+    permuted = jv.permute_symmetric(a, perm)
+    pattern, _ = jv.iluk_pattern(permuted.pattern, k)
+    f = jv.assemble_factors(a, pattern, perm)
+    jv.factor_serial(f)
+    b = np.random.default_rng(3).uniform(-1, 1, a.n)
+    rs, col, val, dg = f.pattern.row_start, f.pattern.col, f.val, f.diag_pos
+    yo = oracle.solve_forward(rs, col, val, b)
+    xo, _ = oracle.solve_backward(rs, col, val, dg, yo)
+    for rep in range(2):
+        y = jv.solve_baseline_csrls(f, b, sched, 8, FORWARD)
+        x = jv.solve_baseline_csrls(f, y, sched, 8, BACKWARD)
+        assert np.array_equal(y, yo) and np.array_equal(x, xo)
