@@ -313,7 +313,7 @@ int jv_classify_solve(int which, int32_t n, const int32_t* row_start, const int3
  * kind 0 and the solve kernels (_kernels.py:348-366) for kinds 1/2. */
 int32_t jv_region_partition_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h,
                                  const int32_t* diag_h, int32_t nreg_max, int32_t max_rows,
-                                 int32_t* region_of_h);
+                                 int32_t dims_max, int32_t* region_of_h);
 int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* row_start_h,
                          const int32_t* col_h, const int32_t* diag_h, const int32_t* region_of_h,
                          int32_t nreg, int32_t threads, int64_t smem_budget, int32_t tau_norms,

@@ -74,7 +74,7 @@ _SIGS = {
     "jv_build_schedule_n": [c_int32, _P, _P, c_int32, c_int32, _P, _P, _P, _I32P, _P],
     "jv_classify_factor": [c_int32, _P, _P, _P, c_int, _P, _P],
     "jv_classify_solve": [c_int, c_int32, _P, _P, _P, _P],
-    "jv_region_partition_host": [c_int32, _P, _P, _P, c_int32, c_int32, _P],
+    "jv_region_partition_host": [c_int32, _P, _P, _P, c_int32, c_int32, c_int32, _P],
     "jv_rstream_build": [c_int32, c_int32, _P, _P, _P, _P, c_int32, c_int32, c_int64, c_int32, _P],
     "jv_rstream_export": [c_int64, _P, _P, _P, _P, _P],
     "jv_pack_values": [c_int64, _P, _P, _P, _P],

@@ -86,19 +86,22 @@ void lifo_order(int32_t n, const std::vector<int64_t>& sptr, const std::vector<i
 }  // namespace
 
 // Acyclic region partition of the lower DAG of a combined L|U pattern.
-// nreg_max regions at most (one CTA per SM), each <= max_rows rows.
+// nreg_max regions at most (one CTA per SM), each <= max_rows rows, refined
+// by at most dims_max (1-3; 0 = 3) orders: 3 gives boxes, 2 pencils.
 // region_of[r] receives the region id; returns the number of regions, or
 // -1 when the rows do not fit (n > nreg * max_rows).
 extern "C" int32_t jv_region_partition_host(int32_t n, const int32_t* rs, const int32_t* col,
                                             const int32_t* diag, int32_t nreg_max,
-                                            int32_t max_rows, int32_t* region_of) {
+                                            int32_t max_rows, int32_t dims_max,
+                                            int32_t* region_of) {
   if (n <= 0 || nreg_max < 1) return -1;
   std::vector<int64_t> sptr;
   std::vector<int32_t> succ, indeg;
   lower_successors(n, rs, col, diag, sptr, succ, indeg);
   int64_t maxs = 0;
   for (int32_t v = 0; v < n; ++v) maxs = std::max(maxs, sptr[v + 1] - sptr[v]);
-  const int dims = (int)std::max<int64_t>(1, std::min<int64_t>(3, maxs));
+  const int dims = (int)std::max<int64_t>(
+      1, std::min<int64_t>(dims_max > 0 ? std::min(dims_max, 3) : 3, maxs));
   // balanced factorisation of <= nreg_max parts into `dims` factors
   int best[3] = {nreg_max, 1, 1};
   int64_t bprod = dims == 1 ? nreg_max : 0;

@@ -26,15 +26,17 @@ def _i32(a):
     return np.ascontiguousarray(a, dtype=np.int32)
 
 
-def partition(row_start, col, diag, nreg_max, max_rows=1 << 15):
-    """(nreg, region_of) of the lower DAG, or None when it does not fit."""
+def partition(row_start, col, diag, nreg_max, max_rows=1 << 15, dims=0):
+    """(nreg, region_of) of the lower DAG, or None when it does not fit.
+    dims: topological orders refining the partition (3 boxes, 2 pencils;
+    0 = up to 3)."""
     rs, cl, dg = _i32(row_start), _i32(col), _i32(diag)
     n = dg.size
     if n == 0:
         return None
     region_of = np.empty(n, np.int32)
     nreg = _lib.load().jv_region_partition_host(n, _p(rs), _p(cl), _p(dg), int(nreg_max),
-                                                int(max_rows), _p(region_of))
+                                                int(max_rows), int(dims), _p(region_of))
     return (int(nreg), region_of) if nreg > 0 else None
 
 
