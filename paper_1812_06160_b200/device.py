@@ -529,36 +529,55 @@ class DevIlu:
 
     def _region_for(self, sweep):
         """The region stream when the region path runs this sweep, else None."""
-        rp = self.region_stream(sweep)
-        if rp is None or self.region_mode == "on":
-            return rp
-        if sweep not in self._rchoice:
-            self._rchoice[sweep] = self._autotune(sweep, rp)
-        return rp if self._rchoice[sweep] else None
+        if not self.use_regions:
+            return None
+        if self.region_mode == "on":
+            return self.region_stream(sweep)
+        key = (sweep, sweep == "factor" and self.tau > 0)
+        if key not in self._rchoice:
+            self._rchoice[key] = self._autotune(sweep)
+        return self._rchoice[key]
 
-    def _autotune(self, sweep, rp):
-        """Time the ticket and the region kernel of one sweep once each
-        (after a warm-up launch) and return True when the region one wins."""
+    def _autotune(self, sweep):
+        """Time the ticket kernel and every region-plan candidate of one sweep
+        once each (after a warm-up launch); keep the fastest (all give the
+        same bits) and free the other plans."""
         t = torch()
+        cands = [None]
+        for c in self.region_candidates.get(sweep, [(0, 0)]):
+            rp = self._stream_for(sweep, c)
+            if rp is not None and all(rp is not x for x in cands):
+                cands.append(rp)
+        if len(cands) == 1:
+            self.autotune_ms[sweep] = ()
+            return None
         ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
         if sweep == "factor":
             save = self.val.clone()
-            runs = [lambda: self._factor_tickets(0, self.n, 0, True),
-                    lambda: self._factor_region(rp, True)]
         else:
             which = 0 if sweep == "fwd" else 1
             vin = t.ones(self.n, dtype=t.float64, device="cuda")
             vout = t.empty_like(vin)
-            runs = [lambda: self._solve_tickets(which, vin, vout),
-                    lambda: self._region_run(rp, 1 + which, vin, vout, self.sbox)]
+
+        def run(rp):
+            if sweep == "factor":
+                if rp is None:
+                    self._factor_tickets(0, self.n, 0, True)
+                else:
+                    self._factor_region(rp, True)
+            elif rp is None:
+                self._solve_tickets(which, vin, vout)
+            else:
+                self._region_run(rp, 1 + which, vin, vout, self.sbox)
+
         times = []
-        for k, fn in enumerate(runs):
+        for rp in cands:
             for rep in range(2):
                 if sweep == "factor":
                     self.val.copy_(save)
                     self.values_changed()
                 ev[2 * rep].record()
-                fn()
+                run(rp)
                 ev[2 * rep + 1].record()
             t.cuda.synchronize()
             times.append(ev[2].elapsed_time(ev[3]))
@@ -567,8 +586,12 @@ class DevIlu:
             self.values_changed()
             _lib.call("jv_reset_row", ptr(self.err), stream())
         check_hang()
+        best = cands[int(np.argmin(times))]
         self.autotune_ms[sweep] = tuple(times)
-        return times[1] < times[0]
+        for k in [k for k, v in self._rstreams.items() if k[0] == sweep and v is not best]:
+            del self._rstreams[k]   # free the losing plans
+        return best
+
     region_min_rows = 64
     region_single_max = 32768   # rows: up to here one region (one CTA) holds the matrix
     region_hint = None
@@ -592,43 +615,55 @@ class DevIlu:
 
     # topological orders refining each sweep's partition (3: boxes, 2:
     # pencils); measured on config 2 the factorization prefers pencils
-    region_dims = {"factor": 2, "fwd": 3, "bwd": 3}
+    # region-plan candidates per sweep: (partition orders: 3 boxes, 2
+    # pencils; region cap, 0 = one per SM).  "on" uses the first; "auto"
+    # times all of them against the ticket kernel (measured: config 2's
+    # factor prefers 144 pencils, its solves 64 pencils; config 3 64 boxes,
+    # config 4 144 boxes)
+    region_candidates = {"factor": [(2, 0), (3, 0)],
+                         "fwd": [(3, 0), (2, 64), (3, 64)], "bwd": [(3, 0), (2, 64), (3, 64)]}
 
-    def regions(self, dims=0):
+    def regions(self, dims=0, rmax=0):
         """(nreg, region_of) or None."""
         if self._regions is None:
             self._regions = {}
-        if dims not in self._regions:
-            self._regions[dims] = self._partition(dims) or False
-        return self._regions[dims] or None
+        if (dims, rmax) not in self._regions:
+            self._regions[(dims, rmax)] = self._partition(dims, rmax) or False
+        return self._regions[(dims, rmax)] or None
 
-    def _partition(self, dims=0):
+    def _partition(self, dims=0, rmax=0):
         if self.region_hint is not None:
             return int(self.region_hint.max()) + 1, self.region_hint
         rs, col, diag = self._host_pattern()
         t = torch()
         sms = t.cuda.get_device_properties(t.cuda.current_device()).multi_processor_count
         # a small matrix fits one CTA: no cross-region hops at all
-        nreg = 1 if self.n <= self.region_single_max else sms
-        return regionplan.partition(rs, col, diag, nreg, dims=dims)
+        nreg = 1 if self.n <= self.region_single_max else min(sms, rmax or sms)
+        return regionplan.partition(rs, col, diag, nreg, max_rows=1 << 20, dims=dims)
 
     def region_stream(self, sweep):
         """Device wave stream of one sweep ("factor", "fwd", "bwd") or None
-        when the region path does not apply."""
+        when the region path does not apply: the autotuned plan if the
+        sweep was tuned, else the first candidate."""
         if not self.use_regions:
             return None
         key = (sweep, sweep == "factor" and self.tau > 0)
+        if key in self._rchoice:
+            return self._rchoice[key]
+        return self._stream_for(sweep, self.region_candidates.get(sweep, [(0, 0)])[0])
+
+    def _stream_for(self, sweep, cand):
+        key = (sweep, cand, sweep == "factor" and self.tau > 0)
         if key not in self._rstreams:
-            self._rstreams[key] = self._build_rstream(sweep) or False
-            self._rchoice.pop(sweep, None)
+            self._rstreams[key] = self._build_rstream(sweep, cand) or False
         return self._rstreams[key] or None
 
-    def _build_rstream(self, sweep):
+    def _build_rstream(self, sweep, cand=(0, 0)):
         if self.n < self.region_min_rows:
             return None
         if sweep == "factor" and self.milu:
             return None
-        reg = self.regions(self.region_dims.get(sweep, 0))
+        reg = self.regions(*cand)
         if reg is None:
             return None
         nreg, region_of = reg

@@ -37,11 +37,13 @@ def timed(fn, reps=5):
     return float(np.median(ts))
 
 
-for dims in (3, 2, 1):
-    ilu.region_dims = {"factor": dims, "fwd": dims, "bwd": dims}
+combos = [(3, 0), (2, 0), (2, 64), (2, 36), (3, 64)]
+for dims, rmax in combos:
+    ilu.region_candidates = {sw: [(dims, rmax)] for sw in ("factor", "fwd", "bwd")}
+    ilu._regions = None
     ilu._rstreams = {}
     ilu._rchoice = {}
-    out = {"cfg": cfg, "dims": dims}
+    out = {"cfg": cfg, "dims": dims, "region_max": rmax}
     if ilu.region_stream("factor") is not None:
         plan.reset_values()
         ilu.factor_async()
