@@ -593,6 +593,7 @@ class DevIlu:
         return best
 
     region_min_rows = 64
+    region_max_rows = 1 << 22   # larger matrices (config 5's 16.7 M-row batch) keep the tickets
     region_single_max = 32768   # rows: up to here one region (one CTA) holds the matrix
     region_hint = None
     KIND = {"factor": 0, "fwd": 1, "bwd": 2}
@@ -659,7 +660,7 @@ class DevIlu:
         return self._rstreams[key] or None
 
     def _build_rstream(self, sweep, cand=(0, 0)):
-        if self.n < self.region_min_rows:
+        if self.n < self.region_min_rows or self.n > self.region_max_rows:
             return None
         if sweep == "factor" and self.milu:
             return None
