@@ -22,11 +22,13 @@ n = ilu.n
 b = dv.f64(np.random.default_rng(0).uniform(-1, 1, n))
 y = dv.empty_f64(n)
 x = dv.empty_f64(n)
-for sw in ("factor", "fwd", "bwd"):
-    ilu.region_stream(sw)
+# the autotuned plans (JV_REGIONS unset) or the first candidates (JV_REGIONS=1)
 plan.reset_values()
 ilu.factor_async()
+ilu.solve_async(0, b, y)
+ilu.solve_async(1, y, x)
 torch.cuda.synchronize()
+print({sw: (ilu._region_for(sw) or {}).get("nreg") for sw in ("factor", "fwd", "bwd")})
 from paper_1812_06160_b200 import _lib
 _lib.call("jv_set_region_flags", int(os.environ.get("JV_RFLAGS", "0")))
 for sw in sweeps:
