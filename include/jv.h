@@ -46,6 +46,11 @@ enum {
 /* ---- context ---------------------------------------------------------- */
 const char* jv_last_error(void);
 int jv_version(void);
+/* page-lock a caller's host buffer in place / release it; async copies on a
+ * stream (kind 0 host->device, 1 device->host): the drop-in API's transfers */
+int jv_host_register(void* ptr, int64_t bytes);
+int jv_host_unregister(void* ptr);
+int jv_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream);
 /* number of SMs and the persistent grid each sync-free kernel uses */
 int jv_device_info(int device, int* sms_h, int* coop_h);
 /* *row = INT32_MAX */

@@ -26,6 +26,9 @@ _I32P = POINTER(c_int32)
 _SIGS = {
     "jv_last_error": [],
     "jv_version": [],
+    "jv_host_register": [_P, c_int64],
+    "jv_host_unregister": [_P],
+    "jv_memcpy_async": [_P, _P, c_int64, c_int, _P],
     "jv_device_info": [c_int, _I32P, _I32P],
     "jv_reset_row": [_P, _P],
     "jv_status": [_I32P],

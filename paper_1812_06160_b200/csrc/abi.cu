@@ -104,6 +104,30 @@ extern "C" const char* jv_last_error(void) { return jvh::g_err; }
 
 extern "C" int jv_version(void) { return 1; }
 
+// Page-lock a caller's host buffer in place (cudaHostRegister), so the
+// drop-in API moves its numpy arrays by DMA with no staging copy.
+// (a failure is reported but cleared from the runtime's error state: the
+// caller falls back to staged copies)
+extern "C" int jv_host_register(void* p, int64_t bytes) {
+  const cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault);
+  if (e == cudaSuccess) return JV_OK;
+  cudaGetLastError();
+  return jvh::cuda_status(e, "jv_host_register");
+}
+extern "C" int jv_host_unregister(void* p) {
+  const cudaError_t e = cudaHostUnregister(p);
+  if (e == cudaSuccess) return JV_OK;
+  cudaGetLastError();
+  return jvh::cuda_status(e, "jv_host_unregister");
+}
+// async copy host <-> device on the caller's stream (kind 0: H2D, 1: D2H)
+extern "C" int jv_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
+  const cudaError_t e = cudaMemcpyAsync(
+      dst, src, (size_t)bytes, kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+      (cudaStream_t)stream);
+  return e == cudaSuccess ? JV_OK : jvh::cuda_status(e, "jv_memcpy_async");
+}
+
 extern "C" int jv_device_info(int device, int* sms_h, int* coop_h) {
   int v = 0;
   cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);

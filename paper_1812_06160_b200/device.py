@@ -94,9 +94,44 @@ def _mark_busy():
     _PIN["busy"] = ev
 
 
+# Large numpy buffers handed to the API are page-locked in place once
+# (cudaHostRegister) and then moved by DMA directly, without the staging
+# copy; the registration is dropped when the array is garbage-collected.
+_REG_MIN = 1 << 22     # bytes
+_REGISTERED = {}       # data pointer -> nbytes
+
+
+def _registered(a):
+    """True when `a` (C-contiguous float64 numpy array) is page-locked."""
+    if a.nbytes < _REG_MIN or not a.flags.c_contiguous or a.base is not None:
+        return False
+    p = a.ctypes.data
+    if _REGISTERED.get(p) == a.nbytes:
+        return True
+    if p in _REGISTERED:
+        return False
+    if _lib.load().jv_host_register(ctypes.c_void_p(p), a.nbytes) != 0:
+        _REGISTERED[p] = -1
+        return False
+    _REGISTERED[p] = a.nbytes
+    import weakref
+
+    def _release(p=p):
+        _lib.load().jv_host_unregister(ctypes.c_void_p(p))
+        _REGISTERED.pop(p, None)
+
+    weakref.finalize(a, _release)
+    return True
+
+
 def upload_f64(dst, src):
     """dst (device tensor) <- src (host float64 numpy array)."""
     t = torch()
+    if isinstance(src, np.ndarray) and src.dtype == np.float64 and _registered(src):
+        _lib.call("jv_memcpy_async", ptr(dst), ctypes.c_void_p(src.ctypes.data), src.nbytes, 0,
+                  stream())
+        sync()   # the caller may reuse its array as soon as we return
+        return dst
     src = np.ascontiguousarray(src, dtype=np.float64)
     n = src.size
     if n == 0:
@@ -116,6 +151,11 @@ def download_f64(dst, src, n=None):
     t = torch()
     n = dst.size if n is None else n
     if n == 0:
+        return dst
+    if dst.dtype == np.float64 and _registered(dst):
+        _lib.call("jv_memcpy_async", ctypes.c_void_p(dst.ctypes.data), ptr(src), 8 * n, 1,
+                  stream())
+        sync()
         return dst
     pin = _pinned(n)
     hdst = t.from_numpy(dst)
