@@ -328,8 +328,8 @@ int jv_rstream_export(int64_t handle, int32_t* words_h, int32_t* table_h, int32_
 /* dst[e] = src[sidx[e]] (0 where sidx < 0): a sweep's wave-ordered values */
 int jv_pack_values(int64_t m, const int32_t* sidx, const double* src, double* dst, void* stream);
 int jv_region_threads(void);
-/* diagnostic switches of the region kernels (bit 0: proxy fence before each
- * static bulk copy, bit 1: no late mailbox re-probes) */
+/* timing diagnostics of the region kernels (results become wrong): 4 skips
+ * the value bulk copies, 8 the remote-dependency waits; 0 in production */
 int jv_set_region_flags(unsigned flags);
 int64_t jv_region_smem_fixed(int32_t max_region, int32_t max_waves);
 int jv_region_run(int32_t kind, int32_t nreg, const void* words, const int32_t* table,
