@@ -115,6 +115,11 @@ JV_INLINE bool bar_test(uint64_t* b, uint32_t parity) {
 JV_INLINE void l2_prefetch_bulk(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+JV_INLINE int ld_acquire_shared(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(sa(p)) : "memory");
+  return v;
+}
 JV_INLINE int ld_volatile_shared(const int* p) {
   int v;
   asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(sa(p)) : "memory");
@@ -226,8 +231,8 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
       }
       if (lo != lo0) {
         if (lane == 0) {
-          __threadfence_block();
-          asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(probed)), "r"(lo) : "memory");
+          // release: the packets written above are visible to whoever acquires
+          asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(sa(probed)), "r"(lo) : "memory");
         }
         ns = 0;
         spins = 0;
@@ -298,9 +303,8 @@ __global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
     // without any passes straight through; the prober never reads its ring
     // blocks, so their reuse needs no handshake)
     if ((tv.w >> 16) > 0) {
-      while (ld_volatile_shared(probed) <= w) {
+      while (ld_acquire_shared(probed) <= w) {
       }
-      __threadfence_block();
     }
     double dv[kR];
     int nd = 0, meta = 0;
