@@ -611,16 +611,19 @@ class DevIlu:
                 self._region_run(rp, 1 + which, vin, vout, self.sbox)
 
         times = []
-        for rp in cands:
-            for rep in range(2):
+        for rp in cands:          # one warm-up launch, then the best of three
+            best = float("inf")
+            for rep in range(4):
                 if sweep == "factor":
                     self.val.copy_(save)
                     self.values_changed()
-                ev[2 * rep].record()
+                ev[0].record()
                 run(rp)
-                ev[2 * rep + 1].record()
-            t.cuda.synchronize()
-            times.append(ev[2].elapsed_time(ev[3]))
+                ev[1].record()
+                t.cuda.synchronize()
+                if rep:
+                    best = min(best, ev[0].elapsed_time(ev[1]))
+            times.append(best)
         if sweep == "factor":
             self.val.copy_(save)
             self.values_changed()
