@@ -1,3 +1,6 @@
+"""Race check of the region forward sweep on a random diagonally dominant
+matrix: five repeated solves, mismatching rows against the oracle.
+(Found the prober / ring-reuse race during development.)"""
 import sys, numpy as np
 sys.path.insert(0, "/root/repo")
 import oracle
