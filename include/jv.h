@@ -183,6 +183,13 @@ int jv_row_norms(int32_t n, const int32_t* row_start, const double* val, double 
                  double* norms, void* stream);
 /* Host-side RCM (ordering.py:199-266) on a symmetrized int32 pattern (host
  * arrays).  Setup only; a device version is the next item. */
+/* Reverse Cuthill-McKee on the device (reference ordering.py:199-266,
+ * bit-exact with jv_rcm_host): symmetrized pattern on the device, perm
+ * (new -> old) written on the device.  Returns 1 (nothing written) when the
+ * graph has more than max_components components of >= 2 vertices: the
+ * level-synchronous traversal would be launch-bound, use jv_rcm_host. */
+int jv_rcm_device(int32_t n, const int32_t* row_start, const int32_t* col, int32_t* perm,
+                  int32_t max_components, int32_t* ncomp_h, void* stream);
 int jv_rcm_host(int32_t n, const int32_t* row_start_h, const int32_t* col_h, int32_t* perm_h);
 /* Host-side level-of-fill ILU(k) for k >= 2 (symbolic.py:86-138); outputs
  * malloc'd (free with jv_free_host); returns nnz or < 0.  k = 1 is device. */

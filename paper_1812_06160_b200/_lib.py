@@ -56,6 +56,7 @@ _SIGS = {
     "jv_assemble": [c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "jv_row_norms": [c_int32, _P, _P, c_double, _P, _P],
     "jv_rcm_host": [c_int32, _P, _P, _P],
+    "jv_rcm_device": [c_int32, _P, _P, _P, c_int32, _I32P, _P],
     "jv_iluk_host": [c_int32, _P, _P, c_int32, POINTER(_I32P), POINTER(_I32P), POINTER(_I32P)],
     "jv_free_host": [c_void_p],
     "jv_factor": [c_int32, _P, _P, _P, _P, _P, c_double, c_int, _P, _P, c_int32, c_int32, _P,

@@ -5,6 +5,7 @@
 #include "factor.cu"
 #include "solve.cu"
 #include "setup.cu"
+#include "rcm.cu"
 #include "elim.cu"
 #include "region.cu"
 #include "regions_host.cpp"

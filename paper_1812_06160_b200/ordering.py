@@ -221,9 +221,36 @@ def level_stats(schedule: LevelSchedule) -> dict:
 def rcm_order(pattern: SparsityPattern) -> Permutation:
     """Reverse Cuthill-McKee on the symmetrized pattern (reference
     ordering.py:199-266): pseudo-peripheral roots from minimum-degree
-    vertices, neighbours by (degree, index), order reversed.  The pattern
-    work runs on the device; the BFS itself in libjv's host C++ (setup-only;
-    a device RCM is the next item)."""
+    vertices, neighbours by (degree, index), order reversed.  On the device
+    (jv_rcm_device: level-synchronous Cuthill-McKee, bit-exact); a graph with
+    more than 64 components of two or more vertices goes to libjv's host C++
+    (jv_rcm_host, same result), where per-component launches would dominate."""
+    n = pattern.n
+    if n == 0:
+        return Permutation(np.zeros(0, dtype=np.int64))
+    sym = symmetrize_pattern(pattern)
+    rs = np.ascontiguousarray(sym.row_start, dtype=np.int32)
+    col = np.ascontiguousarray(sym.col, dtype=np.int32)
+    d = dv.DevCsr.from_host(n, rs, col)
+    perm_d = dv.empty_i32(n)
+    ncomp = ctypes.c_int32(0)
+    rc = _lib.load().jv_rcm_device(n, dv.ptr(d.row_start), dv.ptr(d.col), dv.ptr(perm_d),
+                                   RCM_DEVICE_MAX_COMPONENTS, ctypes.byref(ncomp), dv.stream())
+    if rc == 0:
+        return Permutation(dv.host_i64(perm_d, n))
+    if rc != 1:
+        raise RuntimeError("jv_rcm_device failed: " + _lib.load().jv_last_error().decode())
+    perm = np.empty(n, dtype=np.int32)
+    _lib.call("jv_rcm_host", n, rs.ctypes.data_as(ctypes.c_void_p),
+              col.ctypes.data_as(ctypes.c_void_p), perm.ctypes.data_as(ctypes.c_void_p))
+    return Permutation(perm.astype(np.int64))
+
+
+RCM_DEVICE_MAX_COMPONENTS = 64
+
+
+def rcm_order_host(pattern: SparsityPattern) -> Permutation:
+    """The same ordering computed by libjv's host C++ (jv_rcm_host)."""
     n = pattern.n
     if n == 0:
         return Permutation(np.zeros(0, dtype=np.int64))
