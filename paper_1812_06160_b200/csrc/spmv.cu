@@ -75,6 +75,14 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
     rlast = r1 - 1;
     p1 = __ldg(rs + rlast);
   }
+  // the first summed row's bounds are loaded now, behind the products'
+  // loads, not after the barrier
+  const int rfirst = r0 + threadIdx.x;
+  int ra = 0, rb = 0;
+  if (rfirst < rlast) {
+    ra = __ldg(rs + rfirst);
+    rb = __ldg(rs + rfirst + 1);
+  }
   // products, kU independent load chains per thread in flight (col -> x)
   constexpr int kU = 8;
   for (int b = p0 + threadIdx.x; b < p1; b += kSpmvThreads * kU) {
@@ -95,8 +103,9 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
     }
   }
   __syncthreads();
-  for (int r = r0 + threadIdx.x; r < rlast; r += kSpmvThreads) {
-    const int a = __ldg(rs + r) - p0, b = __ldg(rs + r + 1) - p0;
+  for (int r = rfirst; r < rlast; r += kSpmvThreads) {
+    const int a = (r == rfirst ? ra : __ldg(rs + r)) - p0;
+    const int b = (r == rfirst ? rb : __ldg(rs + r + 1)) - p0;
     double s = 0.0;
     for (int q = a; q < b; ++q) s = jv::dadd(s, prod[q]);
     __stcs(y + (row_map ? __ldg(row_map + r) : r), s);
