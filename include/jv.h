@@ -315,9 +315,10 @@ int jv_classify_solve(int which, int32_t n, const int32_t* row_start, const int3
  *   jv_region_partition_host  region id per row (returns #regions or -1);
  *   jv_rstream_build          wave stream of one direction (kind 0 factor of
  *                             a stencil-class matrix, 1 forward, 2 backward);
- *                             sizes[11] = {static bytes, waves, nreg,
+ *                             sizes[13] = {static bytes, waves, nreg,
  *                             slot ring, max_waves, S, D, CS, CD, remote
- *                             deps, packed values, packed vector};
+ *                             deps, packed values, packed vector,
+ *                             most rows in a wave};
  *                             returns a handle > 0, -1 (a row does not
  *                             qualify) or -2 (shared memory too small);
  *   jv_rstream_export         copies the stream out and frees the handle.
@@ -339,7 +340,8 @@ int jv_region_threads(void);
  * the value bulk copies, 8 the remote-dependency waits; 0 in production */
 int jv_set_region_flags(unsigned flags);
 int64_t jv_region_smem_fixed(int32_t max_region, int32_t max_waves);
-int jv_region_run(int32_t kind, int32_t nreg, const void* words, const int32_t* table,
+int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const void* words,
+                  const int32_t* table,
                   const int32_t* reg_wave, int32_t max_region, int32_t max_waves, int32_t S,
                   int32_t D, int32_t CS, int32_t CD, double* val, const double* pack,
                   const double* vpack, double* out,

@@ -83,7 +83,7 @@ _SIGS = {
     "jv_rstream_export": [c_int64, _P, _P, _P, _P, _P],
     "jv_pack_values": [c_int64, _P, _P, _P, _P],
     "jv_region_smem_fixed": [c_int32, c_int32],
-    "jv_region_run": [c_int32, c_int32, _P, _P, _P, c_int32, c_int32, c_int32, c_int32, c_int32,
+    "jv_region_run": [c_int32, c_int32, c_int32, _P, _P, _P, c_int32, c_int32, c_int32, c_int32, c_int32,
                       c_int32, _P, _P, _P, _P, _P, c_double, _P, c_uint32, _P, _P],
     "jv_region_threads": [],
     "jv_set_region_flags": [ctypes.c_uint],

@@ -133,8 +133,9 @@ JV_INLINE int ld_volatile_shared(const int* p) {
 // all addressed from the wave table alone, up to D waves ahead of the
 // compute warps (whose progress it reads from a shared counter before
 // reusing ring space), with L2 bulk prefetches kL2 waves further ahead.
-template <int KIND>
-__global__ void __launch_bounds__(kBlock, 1) region_kernel(RArgs A) {
+template <int KIND, int NC = kCompute>
+__global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
+  constexpr int kCompute = NC;   // compute threads: waves of at most NC rows
   extern __shared__ __align__(128) unsigned char rsm[];
   const unsigned full = 0xffffffffu;
   const int tid = threadIdx.x;
@@ -427,7 +428,8 @@ extern "C" int64_t jv_region_smem_fixed(int32_t slot_ring, int32_t max_waves) {
   return 256 + 32 * (int64_t)max_waves + 8 * (int64_t)slot_ring;
 }
 
-extern "C" int jv_region_run(int32_t kind, int32_t nreg, const void* words, const int32_t* table,
+extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const void* words,
+                             const int32_t* table,
                              const int32_t* reg_wave, int32_t slot_ring, int32_t max_waves,
                              int32_t S, int32_t D, int32_t CS, int32_t CD, double* val,
                              const double* pack, const double* vpack, double* out, const double* norms, double tau,
@@ -439,13 +441,20 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, const void* words, cons
     return JV_EINVAL;
   }
   const size_t smem = (size_t)jv_region_smem_fixed(slot_ring, max_waves) + CS + CD;
-  const void* fn = kind == 0 ? (const void*)jvr::region_kernel<0>
-                   : kind == 1 ? (const void*)jvr::region_kernel<1>
-                               : (const void*)jvr::region_kernel<2>;
+  // waves of at most 256 rows run on 8 compute warps (cheaper barrier)
+  const bool narrow = max_rows > 0 && max_rows <= 256;
+  const int block = (narrow ? 256 : jvr::kCompute) + 64;
+  const void* fn =
+      narrow ? (kind == 0 ? (const void*)jvr::region_kernel<0, 256>
+                          : kind == 1 ? (const void*)jvr::region_kernel<1, 256>
+                                      : (const void*)jvr::region_kernel<2, 256>)
+             : (kind == 0 ? (const void*)jvr::region_kernel<0>
+                          : kind == 1 ? (const void*)jvr::region_kernel<1>
+                                      : (const void*)jvr::region_kernel<2>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run attr");
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, jvr::kBlock, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem);
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run occupancy");
   if (per_sm * jvh::sm_count() < nreg) {
     jvh::set_error("jv_region_run: %d regions but only %d resident CTAs", nreg,
@@ -456,7 +465,7 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, const void* words, cons
                reg_wave, slot_ring, max_waves, S, D, CS, CD, val, pack, vpack, out, norms, tau, mbox,
                epoch, err_row};
   void* args[] = {&A};
-  e = cudaLaunchCooperativeKernel(fn, dim3(nreg), dim3(jvr::kBlock), args, smem,
+  e = cudaLaunchCooperativeKernel(fn, dim3(nreg), dim3(block), args, smem,
                                   (cudaStream_t)stream);
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run");
   return JV_OK;

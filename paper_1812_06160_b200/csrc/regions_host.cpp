@@ -235,7 +235,7 @@ int32_t min_cap(const std::vector<std::vector<int32_t>>& per_region, int window,
 // smem_budget = shared memory the kernel may use (bytes), tau_norms = the
 // factor gathers each row's norm (tau > 0).  sizes[0..11] receive
 // {static bytes, total waves, nreg, slot ring, max_waves, S, D, CS, CD,
-// remote-dependency count, packed values, packed vector}.  Returns a handle > 0, or
+// remote-dependency count, packed values, packed vector, most rows in a wave}.  Returns a handle > 0, or
 // -1 (a row does not qualify), -2 (does not fit in shared memory).
 extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, const int32_t* col,
                                     const int32_t* diag, const int32_t* region_of, int32_t nreg,
@@ -528,6 +528,11 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   sizes[9] = R->ndeps_remote;
   sizes[10] = (int64_t)R->sidx.size();
   sizes[11] = (int64_t)R->vidx.size();
+  {
+    int64_t mr = 0;
+    for (int64_t w = 0; w < nw; ++w) mr = std::max<int64_t>(mr, wave_cnt[w]);
+    sizes[12] = mr;
+  }
   std::lock_guard<std::mutex> lk(g_rs_mu);
   const int64_t h = g_rs_next++;
   g_rs[h] = std::move(R);

@@ -729,7 +729,7 @@ class DevIlu:
                     vidx=up(ws.vidx) if mv else None, mv=mv,
                     vpack=t.empty(max(mv, 2), dtype=t.float64, device="cuda"),
                     slot_ring=ws.slot_ring, max_waves=ws.max_waves, S=ws.S, D=ws.D, CS=ws.CS,
-                    CD=ws.CD, waves=ws.waves, remote_deps=ws.remote_deps)
+                    CD=ws.CD, waves=ws.waves, remote_deps=ws.remote_deps, max_rows=ws.max_rows)
 
     def values_changed(self):
         """Invalidate the wave-ordered value copies (call after writing val)."""
@@ -748,7 +748,8 @@ class DevIlu:
             src = inp if kind != 0 else self.norms
             _lib.call("jv_pack_values", rp["mv"], ptr(rp["vidx"]), ptr(src), ptr(rp["vpack"]),
                       stream())
-        _lib.call("jv_region_run", kind, rp["nreg"], ptr(rp["words"]), ptr(rp["table"]),
+        _lib.call("jv_region_run", kind, rp["nreg"], rp["max_rows"], ptr(rp["words"]),
+                  ptr(rp["table"]),
                   ptr(rp["reg_wave"]), rp["slot_ring"], rp["max_waves"], rp["S"], rp["D"],
                   rp["CS"], rp["CD"], ptr(self.val), ptr(rp["pack"]), ptr(rp["vpack"]),
                   ptr(out), ptr(self.norms),

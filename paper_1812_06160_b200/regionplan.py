@@ -57,6 +57,7 @@ class WaveStream:
     CS: int
     CD: int
     remote_deps: int
+    max_rows: int = 0        # most rows in one wave
 
     @property
     def waves(self):
@@ -93,7 +94,7 @@ def _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, threa
     kind = KINDS[sweep]
     rs, cl, dg, ro = _i32(row_start), _i32(col), _i32(diag), _i32(region_of)
     threads = min(int(threads), lib.jv_region_threads())
-    sizes = np.zeros(12, np.int64)
+    sizes = np.zeros(13, np.int64)
     h = lib.jv_rstream_build(kind, dg.size, _p(rs), _p(cl), _p(dg), _p(ro), int(nreg), threads,
                              int(smem_budget), int(tau > 0), _p(sizes))
     if h <= 0:
@@ -107,7 +108,8 @@ def _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, threa
               _p(vidx))
     return WaveStream(kind, int(nreg), words, table, sidx[:int(sizes[10])], vidx[:int(sizes[11])],
                       reg_wave, int(sizes[3]),
-                      int(sizes[4]), int(sizes[5]), int(sizes[6]), int(sizes[7]), int(sizes[8]), int(sizes[9]))
+                      int(sizes[4]), int(sizes[5]), int(sizes[6]), int(sizes[7]), int(sizes[8]), int(sizes[9]),
+                      int(sizes[12]))
 
 
 def records(ws: WaveStream, w):
