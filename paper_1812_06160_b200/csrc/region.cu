@@ -441,16 +441,21 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const
     return JV_EINVAL;
   }
   const size_t smem = (size_t)jv_region_smem_fixed(slot_ring, max_waves) + CS + CD;
-  // waves of at most 256 rows run on 8 compute warps (cheaper barrier)
-  const bool narrow = max_rows > 0 && max_rows <= 256;
-  const int block = (narrow ? 256 : jvr::kCompute) + 64;
+  // waves of at most 256 (128) rows run on 8 (4) compute warps: a cheaper
+  // barrier, no idle warps
+  const int nc = max_rows > 0 && max_rows <= 128 ? 128
+                 : max_rows > 0 && max_rows <= 256 ? 256 : jvr::kCompute;
+  const int block = nc + 64;
   const void* fn =
-      narrow ? (kind == 0 ? (const void*)jvr::region_kernel<0, 256>
-                          : kind == 1 ? (const void*)jvr::region_kernel<1, 256>
-                                      : (const void*)jvr::region_kernel<2, 256>)
-             : (kind == 0 ? (const void*)jvr::region_kernel<0>
-                          : kind == 1 ? (const void*)jvr::region_kernel<1>
-                                      : (const void*)jvr::region_kernel<2>);
+      nc == 128 ? (kind == 0 ? (const void*)jvr::region_kernel<0, 128>
+                             : kind == 1 ? (const void*)jvr::region_kernel<1, 128>
+                                         : (const void*)jvr::region_kernel<2, 128>)
+      : nc == 256 ? (kind == 0 ? (const void*)jvr::region_kernel<0, 256>
+                               : kind == 1 ? (const void*)jvr::region_kernel<1, 256>
+                                           : (const void*)jvr::region_kernel<2, 256>)
+                  : (kind == 0 ? (const void*)jvr::region_kernel<0>
+                               : kind == 1 ? (const void*)jvr::region_kernel<1>
+                                           : (const void*)jvr::region_kernel<2>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run attr");
   int per_sm = 0;
