@@ -372,10 +372,12 @@ def run_mine(args):
     from paper_1812_06160_b200 import _lib as _L
     _L.launch_counts.clear()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("timed")   # ncu --nvtx --nvtx-include "timed/"
     t0.record()
     for k in range(args.steps):
         step(evs[k])
     t1.record()
+    torch.cuda.nvtx.range_pop()
     launches = sum(_L.launch_counts.values())
     launch_detail = dict(_L.launch_counts)
     torch.cuda.synchronize()
