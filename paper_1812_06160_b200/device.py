@@ -665,10 +665,10 @@ class DevIlu:
     # region-plan candidates per sweep: (partition orders: 3 boxes, 2
     # pencils; region cap, 0 = one per SM).  "on" uses the first; "auto"
     # times all of them against the ticket kernel (measured: config 2's
-    # factor prefers 144 pencils, its solves 64 pencils; config 3 64 boxes,
+    # factor prefers 144 pencils, its solves 64 pencils; config 3 100 boxes,
     # config 4 144 boxes)
     region_candidates = {"factor": [(2, 0), (3, 0)],
-                         "fwd": [(3, 0), (2, 64), (3, 64)], "bwd": [(3, 0), (2, 64), (3, 64)]}
+                         "fwd": [(3, 0), (2, 64), (3, 100)], "bwd": [(3, 0), (2, 64), (3, 100)]}
 
     def regions(self, dims=0, rmax=0):
         """(nreg, region_of) or None."""

@@ -37,7 +37,7 @@ def timed(fn, reps=5):
     return float(np.median(ts))
 
 
-combos = [(3, 0), (2, 0), (2, 64), (2, 36), (3, 64)]
+combos = [(int(a), int(b)) for a, b in (c.split(',') for c in os.environ.get('JV_COMBOS', '3,0 2,0 2,64 2,36 3,64').split())]
 for dims, rmax in combos:
     ilu.region_candidates = {sw: [(dims, rmax)] for sw in ("factor", "fwd", "bwd")}
     ilu._regions = None
