@@ -131,3 +131,44 @@ def test_csrls_baseline_bitwise(k):
         y = jv.solve_baseline_csrls(f, b, sched, 8, FORWARD)
         x = jv.solve_baseline_csrls(f, y, sched, 8, BACKWARD)
         assert np.array_equal(y, yo) and np.array_equal(x, xo)
+
+
+@pytest.mark.parametrize("mode", ["auto", "on"])
+def test_zero_pivot_any_path(mode):
+    """Whatever path the autotune picks, the smallest zero-pivot row."""
+    a = W.laplace7(14, 2)
+    rs, col, diag, val = _front(a, 0, 0.0)
+    val = val.copy()
+    for r in (700, 1500):
+        val[rs[r]:diag[r] + 1] = 0.0
+    want, bad = oracle.factor_serial(rs, col, val.copy(), diag, 0.0, False)
+    d = dv.DevIlu.from_host(diag.size, rs, col, diag, val)
+    d.region_single_max = 0
+    d.region_mode = mode
+    assert d.factor() == bad == 700
+    upto = rs[bad + 1]
+    assert np.array_equal(d.host_val()[:upto], want[:upto])
+
+
+def test_solves_follow_refactorization():
+    """New values -> factor -> the region solves see the new factors (the
+    wave-ordered value copies are refreshed per factorization)."""
+    a = W.laplace7(12, 6)
+    rs, col, diag, val = _front(a, 0, 0.0)
+    n = diag.size
+    d = dv.DevIlu.from_host(n, rs, col, diag, val)
+    d.region_single_max = 0
+    d.region_mode = "on"
+    b = np.random.default_rng(2).uniform(-1, 1, n)
+    y, x = dv.empty_f64(n), dv.empty_f64(n)
+    for scale in (1.0, 2.0, 0.5):
+        v = val * scale
+        dv.upload_f64(d.val, v)
+        d.values_changed()
+        assert d.factor() == -1
+        want, _ = oracle.factor_serial(rs, col, v.copy(), diag, 0.0, False)
+        d.solve_async(0, dv.f64(b), y)
+        d.solve_async(1, y, x)
+        yo = oracle.solve_forward(rs, col, want, b)
+        xo, _ = oracle.solve_backward(rs, col, want, diag, yo)
+        assert np.array_equal(dv.host_f64(x, n), xo)
