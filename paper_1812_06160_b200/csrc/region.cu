@@ -41,7 +41,7 @@ namespace jvr {
 
 constexpr int kThreads = 512;   // rows per wave (compute threads)
 constexpr int kNB = 16;   // static-block mbarriers in the ring (S + 1 <= kNB)
-constexpr int kL2 = 12;   // waves of L2 bulk prefetch ahead of the gathers
+constexpr int kL2 = 12;   // waves of L2 bulk prefetch ahead of the gathers (24 measured equal)
 
 struct RArgs {
   const int4* words;   // static stream, 16-byte units
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
           }
         }
         slot[me] = d;
-        if (meta & 64) jv::mbox_put(A.mbox, p0 + nd, d, A.epoch);
+        if (meta & 64) jv::mbox_put(A.mbox, V.row(tid), d, A.epoch);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (k < nd) __stcg(A.val + p0 + k, l[k]);

@@ -393,7 +393,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
             v = (slot_of[c] - reg_ptr[g]) % SC;
           } else {
             v = -(1 + (int32_t)pslot.size());
-            pslot.push_back(kind == 0 ? diag[c] : c);   // factor mailbox: diagonal position
+            pslot.push_back(c);   // mailbox slot = row (dense: 8 packets per 128-byte line)
             ++nrem;
           }
           ref[(size_t)(p - lo) * cnt + i] = v;

@@ -161,7 +161,7 @@ def _replay(ws, rs, col, diag, val, vec, tau=0.0, norms=None):
                                 d = d - l * val[_upos(rs, col, diag, r, kk)]
                             val[p0 + kk] = l
                         val[p0 + nd] = d
-                        x, key = d, p0 + nd
+                        x, key = d, r
                     elif kind == 1:
                         s = vec[r]
                         for kk in range(nd):
