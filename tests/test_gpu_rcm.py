@@ -45,3 +45,16 @@ def test_device_rcm_equals_host(name):
     dev = ordering.rcm_order(a.pattern).perm
     assert np.array_equal(np.sort(dev), np.arange(a.n))
     assert np.array_equal(dev, host)
+
+
+def test_many_components_use_host_fallback():
+    """More than RCM_DEVICE_MAX_COMPONENTS multi-vertex components: the
+    device traversal declines (status 1) and the host C++ gives the order."""
+    k = ordering.RCM_DEVICE_MAX_COMPONENTS + 10
+    n = 3 * k
+    r = np.concatenate([np.arange(0, n, 3), np.arange(1, n, 3), np.arange(n)])
+    c = np.concatenate([np.arange(1, n, 3), np.arange(2, n, 3), np.arange(n)])
+    a = CsrMatrix.from_coo(n, np.concatenate([r, c]), np.concatenate([c, r]),
+                           np.ones(2 * r.size))
+    assert np.array_equal(ordering.rcm_order(a.pattern).perm,
+                          ordering.rcm_order_host(a.pattern).perm)
