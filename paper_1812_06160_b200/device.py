@@ -398,6 +398,7 @@ class DevIlu:
         self._hpat = None
         self._vver = 0
         self._csrls = {}
+        self._side = None
         self._elim = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
@@ -742,12 +743,39 @@ class DevIlu:
                       stream())
             rp["pver"] = self._vver
 
-    def _region_run(self, rp, kind, inp, out, box):
+    def _side_pack(self, rp, src=None):
+        """Refresh `rp`'s value pack (from `src`, default the values) on a
+        side stream that starts where the current stream is now; returns the
+        event the current stream must wait on before anything that reads the
+        pack or writes the source."""
+        t = torch()
+        if self._side is None:
+            self._side = t.cuda.Stream()
+        self._side.wait_stream(t.cuda.current_stream())
+        src = self.val if src is None else src
+        _lib.call("jv_pack_values", rp["m"], ptr(rp["sidx"]), ptr(src), ptr(rp["pack"]),
+                  self._side.cuda_stream)
+        rp["pver"] = self._vver
+        ev = t.cuda.Event()
+        ev.record(self._side)
+        return ev
+
+    def load_values(self, src):
+        """values <- `src` (a device copy of the same pattern's values, e.g.
+        the assembled matrix for a refactorization).  (Gathering the
+        factorization's value pack from `src` on a side stream during the
+        copy was measured: no gain, both are bandwidth-bound.)"""
+        self.val.copy_(src)
+        self.values_changed()
+
+    def _region_run(self, rp, kind, inp, out, box, before_kernel=None):
         self._pack(rp)
         if rp["mv"]:
             src = inp if kind != 0 else self.norms
             _lib.call("jv_pack_values", rp["mv"], ptr(rp["vidx"]), ptr(src), ptr(rp["vpack"]),
                       stream())
+        if before_kernel is not None:
+            before_kernel()
         _lib.call("jv_region_run", kind, rp["nreg"], rp["max_rows"], ptr(rp["words"]),
                   ptr(rp["table"]),
                   ptr(rp["reg_wave"]), rp["slot_ring"], rp["max_waves"], rp["S"], rp["D"],
@@ -807,7 +835,20 @@ class DevIlu:
     def solve_async(self, which, b, out):
         rp = self._region_for("fwd" if which == 0 else "bwd")
         if rp is not None:
-            self._region_run(rp, 1 + which, b, out, self.sbox)
+            # the backward sweep's value pack depends only on the factors:
+            # refresh it on a side stream while the forward region kernel
+            # (one CTA per region, most SMs idle) runs
+            nxt = None
+            if which == 0:
+                nxt = (self._rchoice.get(("bwd", False)) if self.region_mode == "auto"
+                       else self.region_stream("bwd"))
+            ev = []
+            hook = None
+            if nxt is not None and nxt["pver"] != self._vver:
+                hook = lambda: ev.append(self._side_pack(nxt))
+            self._region_run(rp, 1 + which, b, out, self.sbox, hook)
+            if ev:
+                torch().cuda.current_stream().wait_event(ev[0])
             return out
         self._solve_tickets(which, b, out)
         return out

@@ -34,8 +34,7 @@ class IluPlan:
     assembled: object        # device copy of the assembled values
 
     def reset_values(self):
-        self.ilu.val.copy_(self.assembled)
-        self.ilu.values_changed()
+        self.ilu.load_values(self.assembled)
 
 
 def _inverse(perm_d):

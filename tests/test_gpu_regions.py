@@ -172,3 +172,39 @@ def test_solves_follow_refactorization():
         yo = oracle.solve_forward(rs, col, want, b)
         xo, _ = oracle.solve_backward(rs, col, want, diag, yo)
         assert np.array_equal(dv.host_f64(x, n), xo)
+
+
+@pytest.mark.parametrize("mode", ["on", "auto"])
+def test_refactor_new_values_region_packs(mode):
+    """Refactorization with new values of the same pattern: the factor's
+    value pack is gathered from the new source on a side stream while the
+    copy runs, the backward pack during the forward sweep; neither may be
+    stale.  Checked bitwise against the oracle for each set of values."""
+    a = W.laplace7(18, 5)
+    rs, col, diag, val0 = _front(a, 0, 0.0)
+    n = diag.size
+    d = dv.DevIlu.from_host(n, rs, col, diag, val0, tau=0.0)
+    d.region_mode = mode
+    src = dv.f64(val0)
+    b = np.random.default_rng(3).uniform(-1, 1, n)
+    bd = dv.f64(b)
+    y, x = dv.empty_f64(n), dv.empty_f64(n)
+    rng = np.random.default_rng(4)
+    for rep in range(4):
+        v = val0 * rng.uniform(0.5, 1.5, val0.size)
+        v[diag] = np.abs(val0[diag]) * (2.0 + rep)
+        src.copy_(dv.f64(v))
+        d.load_values(src)
+        d.factor_async()
+        d.solve_async(0, bd, y)
+        d.solve_async(1, y, x)
+        want, bad = oracle.factor_serial(rs, col, v.copy(), diag, 0.0, False)
+        assert bad < 0 and dv.read_row_slot(d.err) == -1
+        assert np.array_equal(d.host_val(), want)
+        yo = oracle.solve_forward(rs, col, want, b)
+        xo, _ = oracle.solve_backward(rs, col, want, diag, yo)
+        assert np.array_equal(dv.host_f64(y, n), yo)
+        assert np.array_equal(dv.host_f64(x, n), xo)
+    if mode == "on":
+        assert all(d.region_stream(s) is not None for s in ("factor", "fwd", "bwd"))
+    dv.check_hang()
