@@ -176,10 +176,10 @@ def test_solves_follow_refactorization():
 
 @pytest.mark.parametrize("mode", ["on", "auto"])
 def test_refactor_new_values_region_packs(mode):
-    """Refactorization with new values of the same pattern: the factor's
-    value pack is gathered from the new source on a side stream while the
-    copy runs, the backward pack during the forward sweep; neither may be
-    stale.  Checked bitwise against the oracle for each set of values."""
+    """Refactorization with new values of the same pattern: the value packs
+    (the backward one refreshed on a side stream during the forward sweep)
+    may never be stale.  Checked bitwise against the oracle for each set of
+    values."""
     a = W.laplace7(18, 5)
     rs, col, diag, val0 = _front(a, 0, 0.0)
     n = diag.size
@@ -208,3 +208,24 @@ def test_refactor_new_values_region_packs(mode):
     if mode == "on":
         assert all(d.region_stream(s) is not None for s in ("factor", "fwd", "bwd"))
     dv.check_hang()
+
+
+@pytest.mark.parametrize("m", [1, 7, 8, 9, 31, 4096 + 5, 1 << 20])
+def test_pack_values_gather(m):
+    """jv_pack_values: dst[e] = src[sidx[e]], 0 where sidx < 0, every length
+    (full tiles and a partial one)."""
+    from paper_1812_06160_b200 import _lib
+    from paper_1812_06160_b200.device import ptr, stream
+
+    t = dv.torch()
+    rng = np.random.default_rng(m)
+    src = rng.standard_normal(3 * m + 1)
+    sidx = rng.integers(-1, src.size, m).astype(np.int32)
+    want = np.where(sidx >= 0, src[np.maximum(sidx, 0)], 0.0)
+    s_d = dv.f64(src)
+    i_d = t.from_numpy(sidx).cuda()
+    out = t.full((m + 2,), 7.0, dtype=t.float64, device="cuda")
+    _lib.call("jv_pack_values", m, ptr(i_d), ptr(s_d), ptr(out), stream())
+    got = out.cpu().numpy()
+    assert np.array_equal(got[:m], want)
+    assert np.all(got[m:] == 7.0)   # nothing written past m
