@@ -399,6 +399,7 @@ class DevIlu:
         self._vver = 0
         self._csrls = {}
         self._side = None
+        self._sms = None
         self._elim = None
         self._fwd_levels = None
         self.norms = empty_f64(self.n)
@@ -837,9 +838,14 @@ class DevIlu:
         if rp is not None:
             # the backward sweep's value pack depends only on the factors:
             # refresh it on a side stream while the forward region kernel
-            # (one CTA per region, most SMs idle) runs
+            # runs, when that kernel leaves most SMs idle (one CTA per
+            # region; with more regions the pack slows the sweep down more
+            # than it saves: c4 fwd 0.95 -> 1.14 ms)
             nxt = None
-            if which == 0:
+            if self._sms is None:
+                t = torch()
+                self._sms = t.cuda.get_device_properties(t.cuda.current_device()).multi_processor_count
+            if which == 0 and 2 * rp["nreg"] <= self._sms:
                 nxt = (self._rchoice.get(("bwd", False)) if self.region_mode == "auto"
                        else self.region_stream("bwd"))
             ev = []
