@@ -335,6 +335,12 @@ int jv_rstream_export(int64_t handle, int32_t* words_h, int32_t* table_h, int32_
                       int32_t* sidx_h, int32_t* vidx_h);
 /* dst[e] = src[sidx[e]] (0 where sidx < 0): a sweep's wave-ordered values */
 int jv_pack_values(int64_t m, const int32_t* sidx, const double* src, double* dst, void* stream);
+/* two such gathers in one launch (either length may be 0) and, when
+ * reset_row is not NULL, *reset_row = "no row": what runs in front of a
+ * region sweep */
+int jv_pack_values2(int64_t m1, const int32_t* sidx1, const double* src1, double* dst1,
+                    int64_t m2, const int32_t* sidx2, const double* src2, double* dst2,
+                    int32_t* reset_row, void* stream);
 int jv_region_threads(void);
 /* timing diagnostics of the region kernels (results become wrong): 4 skips
  * the value bulk copies, 8 the remote-dependency waits; 0 in production */

@@ -82,6 +82,7 @@ _SIGS = {
     "jv_rstream_build": [c_int32, c_int32, _P, _P, _P, _P, c_int32, c_int32, c_int64, c_int32, _P],
     "jv_rstream_export": [c_int64, _P, _P, _P, _P, _P],
     "jv_pack_values": [c_int64, _P, _P, _P, _P],
+    "jv_pack_values2": [c_int64, _P, _P, _P, c_int64, _P, _P, _P, _P, _P],
     "jv_region_smem_fixed": [c_int32, c_int32],
     "jv_region_run": [c_int32, c_int32, c_int32, _P, _P, _P, c_int32, c_int32, c_int32, c_int32, c_int32,
                       c_int32, _P, _P, _P, _P, _P, c_double, _P, c_uint32, _P, _P],
@@ -124,7 +125,7 @@ def exported_symbols():
 
 # hot-path entry points that launch exactly one kernel of ours per call;
 # launch_counts tallies them (bench.py reports the count it observes)
-_ONE_LAUNCH = {"jv_factor", "jv_solve", "jv_region_run", "jv_pack_values", "jv_row_norms",
+_ONE_LAUNCH = {"jv_factor", "jv_solve", "jv_region_run", "jv_pack_values", "jv_pack_values2", "jv_row_norms",
                "jv_reset_row", "jv_spmv", "jv_spmv_rows", "jv_gather", "jv_check_zero_diag",
                "jv_solve_level"}
 launch_counts = {}

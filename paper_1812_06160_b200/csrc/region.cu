@@ -34,6 +34,8 @@
 // Deadlock freedom: each CTA processes its waves in level order and only
 // waits on rows of lower levels; all CTAs are co-resident (cooperative
 // launch), so the lowest pending level always progresses.
+#include <algorithm>
+
 #include "common.cuh"
 #include "../../include/jv.h"
 
@@ -399,10 +401,11 @@ namespace jvr {
 // warp) and has all E gathers in flight together.
 constexpr int kPackE = 4;
 template <int E>
-__global__ void pack_kernel(int64_t m, const int32_t* __restrict__ sidx, const double* __restrict__ src,
-                            double* __restrict__ dst) {
+__device__ __forceinline__ void pack_tiles(int64_t m, const int32_t* __restrict__ sidx,
+                                           const double* __restrict__ src,
+                                           double* __restrict__ dst, int blk, int nblk) {
   const int64_t tile = (int64_t)E * blockDim.x;
-  for (int64_t t0 = blockIdx.x * tile; t0 < m; t0 += gridDim.x * tile) {
+  for (int64_t t0 = blk * tile; t0 < m; t0 += nblk * tile) {
     int k[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -419,21 +422,52 @@ __global__ void pack_kernel(int64_t m, const int32_t* __restrict__ sidx, const d
     }
   }
 }
+struct PackJob {
+  int64_t m;
+  const int32_t* sidx;
+  const double* src;
+  double* dst;
+};
+// two gathers in one launch (blocks [0, g1) do the first), and optionally
+// an error-row slot reset: the launches in front of a region sweep
+template <int E>
+__global__ void pack_kernel(PackJob a, PackJob b, int g1, int32_t* reset) {
+  if (reset && blockIdx.x == 0 && threadIdx.x == 0) *reset = jv::kNoRow;
+  if ((int)blockIdx.x < g1) pack_tiles<E>(a.m, a.sidx, a.src, a.dst, blockIdx.x, g1);
+  else pack_tiles<E>(b.m, b.sidx, b.src, b.dst, blockIdx.x - g1, gridDim.x - g1);
+}
 }  // namespace jvr
 
 // dst[e] = src[sidx[e]] (0 where sidx < 0): the wave-ordered value arrays
 // of the region kernels, refreshed once per factorization
-extern "C" int jv_pack_values(int64_t m, const int32_t* sidx, const double* src, double* dst,
-                              void* stream) {
-  if (m <= 0) return JV_OK;
+extern "C" int jv_pack_values2(int64_t m1, const int32_t* sidx1, const double* src1, double* dst1,
+                               int64_t m2, const int32_t* sidx2, const double* src2, double* dst2,
+                               int32_t* reset_row, void* stream) {
+  if (m1 < 0 || m2 < 0) {
+    jvh::set_error("jv_pack_values2: negative length");
+    return JV_EINVAL;
+  }
+  if (m1 == 0 && m2 == 0 && !reset_row) return JV_OK;
   // (measured at c2: 4 elements per thread, factor span 502 -> 487 us;
   // 1: 502, 2: 490, 8: 498; grid cap 4 / 8 / 16 blocks per SM: 494 / 487 / 489)
-  int64_t grid = (m + jvr::kPackE * 256 - 1) / (jvr::kPackE * 256);
-  if (grid < 1) grid = 1;
-  if (grid > 8 * jvh::sm_count()) grid = 8 * jvh::sm_count();
-  jvr::pack_kernel<jvr::kPackE><<<(int)grid, 256, 0, (cudaStream_t)stream>>>(m, sidx, src, dst);
-  JV_CHECK_LAUNCH("jv_pack_values");
+  const int64_t tile = jvr::kPackE * 256, cap = 8 * (int64_t)jvh::sm_count();
+  int64_t g1 = (m1 + tile - 1) / tile, g2 = (m2 + tile - 1) / tile;
+  if (g1 + g2 > cap) {   // share the cap in proportion, at least one block per job
+    const int64_t c1 = m1 ? std::max<int64_t>(1, cap * m1 / (m1 + m2)) : 0;
+    g2 = m2 ? std::max<int64_t>(1, std::min(g2, cap - c1)) : 0;
+    g1 = std::min(g1, c1);
+  }
+  const int64_t grid = std::max<int64_t>(1, g1 + g2);
+  jvr::pack_kernel<jvr::kPackE><<<(int)grid, 256, 0, (cudaStream_t)stream>>>(
+      jvr::PackJob{m1, sidx1, src1, dst1}, jvr::PackJob{m2, sidx2, src2, dst2}, (int)g1,
+      reset_row);
+  JV_CHECK_LAUNCH("jv_pack_values2");
   return JV_OK;
+}
+
+extern "C" int jv_pack_values(int64_t m, const int32_t* sidx, const double* src, double* dst,
+                              void* stream) {
+  return jv_pack_values2(m, sidx, src, dst, 0, nullptr, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int jv_region_threads(void) { return jvr::kThreads; }

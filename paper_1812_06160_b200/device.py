@@ -769,12 +769,19 @@ class DevIlu:
         self.val.copy_(src)
         self.values_changed()
 
-    def _region_run(self, rp, kind, inp, out, box, before_kernel=None):
-        self._pack(rp)
-        if rp["mv"]:
-            src = inp if kind != 0 else self.norms
-            _lib.call("jv_pack_values", rp["mv"], ptr(rp["vidx"]), ptr(src), ptr(rp["vpack"]),
-                      stream())
+    def _region_run(self, rp, kind, inp, out, box, before_kernel=None, reset=None):
+        # one launch in front of the sweep: its value pack when stale, the
+        # per-call vector pack, the error-row reset
+        m1 = 0
+        if rp["pver"] != self._vver:
+            m1 = rp["m"]
+            rp["pver"] = self._vver
+        m2 = rp["mv"]
+        vsrc = (inp if kind != 0 else self.norms) if m2 else None
+        if m1 or m2 or reset is not None:
+            _lib.call("jv_pack_values2", m1, ptr(rp["sidx"]), ptr(self.val), ptr(rp["pack"]),
+                      m2, ptr(rp["vidx"]) if m2 else None, ptr(vsrc), ptr(rp["vpack"]) if m2 else None,
+                      ptr(reset), stream())
         if before_kernel is not None:
             before_kernel()
         _lib.call("jv_region_run", kind, rp["nreg"], rp["max_rows"], ptr(rp["words"]),
@@ -799,8 +806,7 @@ class DevIlu:
     def _factor_region(self, rp, norms):
         if norms and self.tau > 0:
             self.compute_norms()
-        _lib.call("jv_reset_row", ptr(self.err), stream())
-        self._region_run(rp, 0, None, None, self.fbox)
+        self._region_run(rp, 0, None, None, self.fbox, reset=self.err)
 
     def _factor_tickets(self, lo, hi, ready_below, norms):
         sched = self.factor_schedule()

@@ -229,3 +229,30 @@ def test_pack_values_gather(m):
     got = out.cpu().numpy()
     assert np.array_equal(got[:m], want)
     assert np.all(got[m:] == 7.0)   # nothing written past m
+
+
+@pytest.mark.parametrize("m1,m2", [(0, 0), (0, 9), (13, 0), (5000, 3), (1 << 21, 1 << 20),
+                                   (7, 1 << 22)])
+def test_pack_values2_two_jobs_and_reset(m1, m2):
+    """jv_pack_values2: both gathers (the launch grid split between them,
+    capped) and the error-row reset in one launch."""
+    from paper_1812_06160_b200 import _lib
+    from paper_1812_06160_b200.device import ptr, stream
+
+    t = dv.torch()
+    rng = np.random.default_rng(m1 * 7 + m2)
+    jobs = []
+    for m in (m1, m2):
+        src = rng.standard_normal(2 * m + 3)
+        sidx = rng.integers(-1, src.size, m).astype(np.int32)
+        want = np.where(sidx >= 0, src[np.maximum(sidx, 0)], 0.0)
+        out = t.full((m + 1,), 5.0, dtype=t.float64, device="cuda")
+        jobs.append((dv.f64(src), t.from_numpy(sidx).cuda(), out, want, m))
+    slot = t.zeros(1, dtype=t.int32, device="cuda")
+    (s1, i1, o1, _, _), (s2, i2, o2, _, _) = jobs
+    _lib.call("jv_pack_values2", m1, ptr(i1), ptr(s1), ptr(o1), m2, ptr(i2), ptr(s2), ptr(o2),
+              ptr(slot), stream())
+    for _, _, out, want, m in jobs:
+        got = out.cpu().numpy()
+        assert np.array_equal(got[:m], want) and got[m] == 5.0
+    assert dv.read_row_slot(slot) == -1   # reset to "no row"
