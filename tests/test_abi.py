@@ -40,3 +40,37 @@ def test_loader_sets_signatures():
     assert lib.jv_version() == 1
     assert lib.jv_spmv_tile() > 0
     assert isinstance(lib.jv_last_error(), bytes)
+
+
+def _status(lib, fn, *args):
+    rc = getattr(lib, fn)(*args)
+    return rc, lib.jv_last_error()
+
+
+def test_bad_arguments_are_rejected_before_any_device_work():
+    """Argument checks run first and report JV_EINVAL (-1) with a message
+    naming the entry point; no CUDA call is made, so this runs without a GPU."""
+    lib = _lib.load()
+    cases = [
+        ("jv_spmv", (-1, 0, None, None, None, None, None, None, None)),
+        ("jv_spmv", (4, -5, None, None, None, None, None, None, None)),
+        ("jv_pack_values2", (-1, None, None, None, 0, None, None, None, None, None)),
+        ("jv_levels", (0, -1, None, None, None, None, 1, None, None)),
+        ("jv_levels", (0, 4, None, None, None, None, 0, None, None)),   # epoch 0 is reserved
+        ("jv_level_sort", (-1, 0, None, None, None, None)),
+        ("jv_dot", (-1, None, None, None, None, 0, None)),
+        ("jv_set_sfp_group", (3,)),
+        ("jv_set_sfp_group", (64,)),
+    ]
+    for fn, args in cases:
+        rc, msg = _status(lib, fn, *args)
+        assert rc == -1, (fn, args, rc)
+        assert fn.encode() in msg or b"bad" in msg, (fn, msg)
+
+
+def test_empty_inputs_are_no_ops():
+    """n == 0 (and an empty pack without a reset slot) return JV_OK without
+    launching anything, as the reference's loops do nothing on empty input."""
+    lib = _lib.load()
+    assert lib.jv_spmv(0, 0, None, None, None, None, None, None, None) == 0
+    assert lib.jv_pack_values2(0, None, None, None, 0, None, None, None, None, None) == 0
