@@ -354,6 +354,35 @@ int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const void* word
                   const double* norms, double tau, uint64_t* mbox, uint32_t epoch,
                   int32_t* err_row, void* stream);
 
+/* ---- lower-tail two-stage factorization (a20) ------------------------
+ * Replaces the reference's SR / ER lower stage (lower.py:273-318 ->
+ * factor_sr_kernel _kernels.py:326-343, factor_er_kernel :221-228) and the
+ * corner (factor_corner_kernel :231-240).  Rows [n_upper, n) of the
+ * level-ordered factor storage; the upper rows must be factored.
+ *
+ * jv_tail_plan_build: pattern-only plan (device), returns a handle > 0 or a
+ *   negative status.  MILU changes the update lists, tau does not.
+ * jv_tail_plan_info: info[6] = {tail rows, upper-pivot L positions,
+ *   updates, groups, segments, corner entries}.
+ * jv_tail_upper: stage 1, every tail row eliminates its upper-stage
+ *   pivots (warp per row; DIVIDE per group of independent pivots, UPDATE as
+ *   a segmented reduction, one lane per target in pivot order: bitwise the
+ *   reference's sequence).  norms: row inf-norms of the ORIGINAL tail
+ *   values (needed when tau > 0).
+ * jv_tail_corner: the corner (tail rows x columns >= n_upper) as a compact
+ *   CSR (columns shifted by -n_upper) plus the storage position of each
+ *   entry, for the sync-free factor of the corner and the scatter back.
+ * jv_scatter: dst[idx[i]] = src[i]. */
+int64_t jv_tail_plan_build(int32_t n, int32_t n_upper, const int32_t* row_start,
+                           const int32_t* col, const int32_t* diag_pos, int milu, void* stream);
+int jv_tail_plan_info(int64_t handle, int64_t* info_h);
+int jv_tail_upper(int64_t handle, const int32_t* col, const int32_t* diag_pos, double* val,
+                  const double* norms, double tau, void* stream);
+int jv_tail_corner(int64_t handle, int32_t* row_start, int32_t* col, int32_t* diag_pos,
+                   int32_t* pos, void* stream);
+int jv_tail_plan_free(int64_t handle);
+int jv_scatter(int64_t n, const int32_t* idx, const double* src, double* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

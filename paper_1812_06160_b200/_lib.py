@@ -88,6 +88,12 @@ _SIGS = {
                       c_int32, _P, _P, _P, _P, _P, c_double, _P, c_uint32, _P, _P],
     "jv_region_threads": [],
     "jv_set_region_flags": [ctypes.c_uint],
+    "jv_tail_plan_build": [c_int32, c_int32, _P, _P, _P, c_int, _P],
+    "jv_tail_plan_info": [c_int64, POINTER(c_int64)],
+    "jv_tail_upper": [c_int64, _P, _P, _P, _P, c_double, _P],
+    "jv_tail_corner": [c_int64, _P, _P, _P, _P, _P],
+    "jv_tail_plan_free": [c_int64],
+    "jv_scatter": [c_int64, _P, _P, _P, _P],
 }
 _RESTYPES = {
     "jv_last_error": ctypes.c_char_p,
@@ -96,6 +102,7 @@ _RESTYPES = {
     "jv_region_partition_host": c_int32,
     "jv_rstream_build": c_int64,
     "jv_region_smem_fixed": c_int64,
+    "jv_tail_plan_build": c_int64,
 }
 
 _lib = None
@@ -127,7 +134,7 @@ def exported_symbols():
 # launch_counts tallies them (bench.py reports the count it observes)
 _ONE_LAUNCH = {"jv_factor", "jv_solve", "jv_region_run", "jv_pack_values", "jv_pack_values2", "jv_row_norms",
                "jv_reset_row", "jv_spmv", "jv_spmv_rows", "jv_gather", "jv_check_zero_diag",
-               "jv_solve_level"}
+               "jv_solve_level", "jv_tail_upper", "jv_scatter"}
 launch_counts = {}
 
 

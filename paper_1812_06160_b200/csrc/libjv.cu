@@ -7,6 +7,7 @@
 #include "setup.cu"
 #include "rcm.cu"
 #include "elim.cu"
+#include "tail.cu"
 #include "region.cu"
 #include "regions_host.cpp"
 #include "blas.cu"

@@ -235,6 +235,44 @@ def check_hang():
         raise RuntimeError("a sync-free kernel wait timed out (schedule does not cover a dependency)")
 
 
+# ------------------------------------------------------------- tail plan
+
+
+# autotune candidate of the factorization: upper rows by the sync-free
+# kernel, then the two-stage lower tail (csrc/tail.cu)
+TWO_STAGE = {"two_stage": True, "nreg": 0}
+
+
+class TailPlan:
+    """Device plan of the lower tail (jv_tail_plan_build): update lists of
+    stage 1 and the compact corner as its own DevIlu (structure only)."""
+
+    def __init__(self, ilu, n_upper):
+        import weakref
+        lib = _lib.load()
+        h = lib.jv_tail_plan_build(ilu.n, n_upper, ptr(ilu.row_start), ptr(ilu.col),
+                                   ptr(ilu.diag_pos), int(ilu.milu), stream())
+        if h <= 0:
+            raise RuntimeError(f"jv_tail_plan_build failed ({h}): "
+                               f"{lib.jv_last_error().decode(errors='replace')}")
+        self.h = h
+        self._fin = weakref.finalize(self, lib.jv_tail_plan_free, h)
+        info = (ctypes.c_int64 * 6)()
+        _lib.call("jv_tail_plan_info", h, info)
+        self.nt, self.nl, self.nops, self.ngroups, self.nsegs, self.nc = (int(v) for v in info)
+        self.n_upper = n_upper
+        self.corner = None
+        if self.nt:
+            rs = empty_i32(self.nt + 1)
+            col = empty_i32(self.nc)
+            dg = empty_i32(self.nt)
+            self.pos = empty_i32(self.nc)
+            _lib.call("jv_tail_corner", h, ptr(rs), ptr(col), ptr(dg), ptr(self.pos), stream())
+            self.crs = host_i64(rs, self.nt + 1)
+            self.corner = DevIlu(self.nt, rs, col, dg)
+            self.save = empty_f64(self.nc)
+
+
 # ------------------------------------------------------------------ CSR
 
 
@@ -402,6 +440,8 @@ class DevIlu:
         self._sms = None
         self._elim = None
         self._fwd_levels = None
+        self.holder = None      # whose values `val` holds (IluFactors / IluPreconditioner)
+        self.n_upper = None     # first lower-tail row (set by the device plan)
         self.norms = empty_f64(self.n)
         self.fbox = Mailbox(self.nnz, 2)
         self.sbox = Mailbox(self.n, 2)
@@ -590,6 +630,8 @@ class DevIlu:
             rp = self._stream_for(sweep, c)
             if rp is not None and all(rp is not x for x in cands):
                 cands.append(rp)
+        if sweep == "factor" and self.n_upper is not None and 0 < self.n_upper < self.n:
+            cands.append(TWO_STAGE)
         if len(cands) == 1:
             self.autotune_ms[sweep] = ()
             return None
@@ -605,6 +647,8 @@ class DevIlu:
             if sweep == "factor":
                 if rp is None:
                     self._factor_tickets(0, self.n, 0, True)
+                elif rp is TWO_STAGE:
+                    self.factor_two_stage_async(self.n_upper)
                 else:
                     self._factor_region(rp, True)
             elif rp is None:
@@ -636,7 +680,8 @@ class DevIlu:
         k = int(np.argmin(times))
         best = cands[k] if times[k] < 0.97 * times[0] else None
         self.autotune_ms[sweep] = tuple(times)
-        for k in [k for k, v in self._rstreams.items() if k[0] == sweep and v is not best]:
+        for k in [k for k, v in self._rstreams.items() if k[0] == sweep and v is not best
+                  and v is not TWO_STAGE]:
             del self._rstreams[k]   # free the losing plans
         return best
 
@@ -796,6 +841,9 @@ class DevIlu:
         hi = self.n if hi is None else hi
         if lo == 0 and hi == self.n and ready_below == 0:
             rp = self._region_for("factor")
+            if rp is TWO_STAGE:
+                self.factor_two_stage_async(self.n_upper)
+                return
             if rp is not None:
                 self._factor_region(rp, norms)
                 self.values_changed()
@@ -813,7 +861,10 @@ class DevIlu:
         el = self.elim_lists()
         hub = self.hub_plans()
         if lo > 0 or hi < self.n:
-            sched = sched.restrict(lo, hi)
+            key = (lo, hi, id(sched))
+            if getattr(self, "_sub", None) is None or self._sub[0] != key:
+                self._sub = (key, sched.restrict(lo, hi))
+            sched = self._sub[1]
         if norms:
             self.compute_norms()
         _lib.call("jv_reset_row", ptr(self.err), stream())
@@ -825,6 +876,67 @@ class DevIlu:
                   ptr(el[2]) if el else None,
                   ptr(sched.batch_class()) if sched.nbatch else None,
                   *([ptr(x) for x in hub[:4]] if hub else [None] * 4), stream())
+
+    # lower-tail two-stage factorization (csrc/tail.cu) ----------------
+    def tail_plan(self, n_upper):
+        """Plan of the lower tail rows [n_upper, n) (cached per n_upper and
+        MILU flag): stage-1 update lists and the compact corner."""
+        key = (int(n_upper), bool(self.milu))
+        if getattr(self, "_tail", None) is None or self._tail[0] != key:
+            self._tail = (key, TailPlan(self, int(n_upper)))
+        return self._tail[1]
+
+    def factor_tail_async(self, n_upper, norms=True):
+        """Two-stage lower tail (lower.py:273-318): stage 1 eliminates every
+        tail row's upper-stage pivots (jv_tail_upper, segmented, one warp
+        per row), stage 2 factors the corner with the sync-free kernel on
+        its compact copy and scatters it back.  Rows < n_upper must be
+        factored.  The corner's error slot holds the corner row (or none)."""
+        tp = self.tail_plan(n_upper)
+        if tp.nt == 0:
+            return tp
+        if norms and self.tau > 0:
+            self.compute_norms()
+        _lib.call("jv_tail_upper", tp.h, ptr(self.col), ptr(self.diag_pos), ptr(self.val),
+                  ptr(self.norms), self.tau, stream())
+        c = tp.corner
+        if tp.nc:
+            _lib.call("jv_gather", tp.nc, ptr(tp.pos), ptr(self.val), ptr(c.val), stream())
+            tp.save.copy_(c.val[:tp.nc])
+        c.values_changed()
+        if self.tau > 0:
+            c.norms[:tp.nt].copy_(self.norms[n_upper:self.n])
+        c.tau, c.milu = self.tau, self.milu
+        c._factor_tickets(0, tp.nt, 0, False)
+        if tp.nc:
+            _lib.call("jv_scatter", tp.nc, ptr(tp.pos), ptr(c.val), ptr(self.val), stream())
+        self.values_changed()
+        return tp
+
+    def factor_tail(self, n_upper):
+        """factor_tail_async + the reference's error semantics: the smallest
+        zero-pivot row (or -1); rows after it keep their stage-1 values, as
+        the serial corner kernel stops there (_kernels.py:231-240)."""
+        tp = self.factor_tail_async(n_upper)
+        if tp.nt == 0:
+            return -1
+        bad = read_row_slot(tp.corner.err)
+        check_hang()
+        if bad < 0:
+            return -1
+        k = int(tp.crs[bad + 1])
+        if k < tp.nc:
+            _lib.call("jv_scatter", tp.nc - k, ctypes.c_void_p(tp.pos.data_ptr() + 4 * k),
+                      ctypes.c_void_p(tp.save.data_ptr() + 8 * k), ptr(self.val), stream())
+        self.values_changed()
+        return n_upper + bad
+
+    def factor_two_stage_async(self, n_upper):
+        """Upper rows with the sync-free kernel, then the lower tail."""
+        if n_upper > 0:
+            self._factor_tickets(0, n_upper, 0, True)
+        self.factor_tail_async(n_upper, norms=(n_upper == 0))
+        self.values_changed()
 
     def factor(self, lo=0, hi=None, ready_below=0):
         """Factor and return the smallest zero-pivot row (or -1)."""

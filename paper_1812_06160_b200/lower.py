@@ -4,10 +4,13 @@ level scheduling — the reference lower.py API
 
 On the CPU the reference offers two methods for the tail (Segmented-Rows
 tiles and Even-Rows chunks, then the corner).  On the GPU both become the
-same sync-free kernel launch over the tail rows (jv_factor with
-ready_below = n_upper): upper-stage pivots are read as final values, corner
-pivots are awaited through the mailbox.  The result is bitwise equal to
-factor_serial either way, exactly as both reference methods are.  The
+same two launches (csrc/tail.cu): the segmented upper-pivot stage over all
+tail rows at once (warp per row; DIVIDE over groups of independent pivots,
+UPDATE as a segmented reduction with one lane per target position folding
+its updates in pivot order), then the corner — the tail rows restricted to
+columns >= n_upper — by the sync-free factor kernel on a compact copy.  The
+result is bitwise equal to factor_serial either way, exactly as both
+reference methods are.  The
 layouts (TileLayout, ER chunks) are still built with the reference's rules
 because they are part of the API and of the solve setup.
 """
@@ -196,9 +199,19 @@ def er_chunks(pattern: SparsityPattern, n_upper: int, nthreads: int) -> np.ndarr
 
 
 def _factor_tail(factors: IluFactors, n_upper: int) -> None:
-    from .factor import _run
+    """Both reference methods (SR tiles, ER chunks) on the GPU: stage 1 is
+    the segmented upper-pivot elimination of every tail row (jv_tail_upper:
+    warp per row, groups of independent pivots divided in parallel, each
+    target's updates folded in pivot order — the SR kernel's DIVIDE/UPDATE
+    with per-row groups), stage 2 the corner by the sync-free kernel on its
+    compact copy.  Bitwise equal to factor_serial; after a zero pivot the
+    later corner rows keep their stage-1 values, as in the reference."""
+    from . import device as dv
 
-    bad = _run(factors, lo=n_upper, hi=factors.n, ready_below=n_upper)
+    d = factors.upload_values()
+    bad = d.factor_tail(n_upper)
+    factors.val = np.ascontiguousarray(factors.val, dtype=np.float64)
+    dv.download_f64(factors.val, d.val, factors.pattern.nnz)
     if bad >= 0:
         raise ZeroPivotError(int(bad))
 

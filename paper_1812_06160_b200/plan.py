@@ -95,5 +95,6 @@ def build_plan(a: CsrMatrix, base_perm=None, k: int = 0, tau: float = 0.0, milu:
     if bad_diag >= 0:
         raise MissingDiagonalError(bad_diag)
     ilu = dv.DevIlu(n, fpat.row_start, fpat.col, diag, val, tau, milu)
+    ilu.n_upper = n_upper
     return IluPlan(n, base, level_of, nlev, cut, n_upper, total, permuted, fill, ilu,
                    val.clone())

@@ -80,6 +80,7 @@ class IluFactors:
         if self.pattern.nnz:
             dv.upload_f64(d.val, self.val)
         d.values_changed()
+        d.holder = self
         return d
 
 

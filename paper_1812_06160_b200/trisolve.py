@@ -45,6 +45,16 @@ def _check_which(which: str) -> None:
         raise ValueError(f"which must be 'forward' or 'backward', got {which!r}")
 
 
+def _check_schedule(factors: IluFactors, schedule, partition=None) -> None:
+    """The GPU sweeps do not read the CPU wait lists, but a schedule (or
+    partition) built for another matrix is still an error, as it would be
+    for the reference's kernels that index by it."""
+    if schedule is not None and np.asarray(schedule.owner).size != factors.n:
+        raise ConfigurationError("sync schedule does not match the factors")
+    if partition is not None and partition.n != factors.n:
+        raise ConfigurationError("stage partition does not match the factors")
+
+
 def _device_sweep(factors: IluFactors, b: np.ndarray, which: str) -> np.ndarray:
     b = np.array(b, dtype=np.float64, copy=True)
     if factors.n == 0:
@@ -101,6 +111,7 @@ def solve_ls(
 ) -> np.ndarray:
     """Point-to-point solve entry point (trisolve.py:111-137)."""
     _check_which(which)
+    _check_schedule(factors, schedule)
     return _device_sweep(factors, b, which)
 
 
@@ -115,6 +126,7 @@ def solve_ls_lower(
 ) -> np.ndarray:
     """Two-stage solve entry point (trisolve.py:140-182)."""
     _check_which(which)
+    _check_schedule(factors, schedule, partition)
     return _device_sweep(factors, b, which)
 
 

@@ -135,6 +135,10 @@ CONFIGS = {
     "c2": dict(name="laplace7_128_rcm", k=0, tau=0.0, order="rcm", min_level_rows=16),
     "c3": dict(name="convdiff7_96_ilu1_tau1e-3", k=1, tau=1e-3, order="natural",
                min_level_rows=16),
+    # c3 with tau = 1e-2: the variant where drops fire at full size
+    # (tau = 1e-3 drops nothing on this matrix)
+    "c3t": dict(name="convdiff7_96_ilu1_tau1e-2", k=1, tau=1e-2, order="natural",
+                min_level_rows=16),
     "c4": dict(name="stencil27_100_nd", k=0, tau=0.0, order="file", min_level_rows=256),
     "c5": dict(name="rmat18_x64", k=0, tau=0.0, order="natural", min_level_rows=16),
 }
@@ -274,7 +278,7 @@ def config_matrix(cfg: str, scale: float = 1.0, rmat_count: int = 64):
     elif cfg == "c2":
         k = max(4, int(round(128 * scale)))
         a, base = laplace7(k), "rcm"
-    elif cfg == "c3":
+    elif cfg in ("c3", "c3t"):
         k = max(4, int(round(96 * scale)))
         a, base = convdiff3d(k), None
     elif cfg == "c4":

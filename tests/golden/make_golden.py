@@ -157,7 +157,7 @@ def make_small(path):
 # ----------------------------------------------------------------- full
 
 
-def make_full(path, which):
+def make_full(path, which, c5_seeds=(0, 1)):
     from paper_1812_06160_b200 import workloads as W
 
     result = json.load(open(path)) if os.path.exists(path) else {}
@@ -166,7 +166,7 @@ def make_full(path, which):
         s = W.CONFIGS[cfg]
         mats = []
         if cfg == "c5":
-            for seed in (0, 1):
+            for seed in c5_seeds:
                 mats.append((f"c5_seed{seed}", W.rmat(18, seed), None))
         else:
             a, base, _ = W.config_matrix(cfg)
@@ -197,6 +197,8 @@ def make_full(path, which):
                 xbad=int(res["xbad"]), fwd_depth=int(res["fwd_lev"].max() + 1),
                 bwd_depth=int(res["bwd_lev"].max() + 1),
                 dropped=int(np.sum((res["fval"] == 0.0) & low & (res["assembled"] != 0.0))),
+                # L positions left exactly 0 (dropped multipliers, fill included)
+                zero_l=int(np.sum((res["fval"] == 0.0) & low)),
                 k=s["k"], tau=s["tau"], min_level_rows=s["min_level_rows"],
                 x_absmax=float(np.max(np.abs(res["x"]))),
                 fval_absmax=float(np.max(np.abs(res["fval"]))),
@@ -210,8 +212,12 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--full", default="")
+    ap.add_argument("--c5-seeds", default="0-1", help="R-MAT seeds for c5, e.g. 0-63")
+    ap.add_argument("--out", default=os.path.join(HERE, "full_digests.json"))
     args = ap.parse_args()
+    lo, _, hi = args.c5_seeds.partition("-")
+    seeds = range(int(lo), int(hi or lo) + 1)
     if args.small:
         make_small(os.path.join(HERE, "small.npz"))
     if args.full:
-        make_full(os.path.join(HERE, "full_digests.json"), args.full.split(","))
+        make_full(args.out, args.full.split(","), seeds)

@@ -51,6 +51,13 @@ def check(key, a, base_perm):
     assert h(ilu.host_val(), "f") == want["assembled"]
     assert ilu.factor() == st["bad"]
     assert h(ilu.host_val(), "f") == want["fval"]
+    if plan.n_upper < n:
+        # the two-stage path (upper stage + segmented lower tail + corner)
+        plan.reset_values()
+        ilu.factor_two_stage_async(plan.n_upper)
+        assert h(ilu.host_val(), "f") == want["fval"], "two-stage factor differs"
+        plan.reset_values()
+        assert ilu.factor() == st["bad"]
     perm = dv.host_i64(plan.perm, n)
     b = np.random.default_rng(0).uniform(-1.0, 1.0, n)[perm]
     bd = dv.f64(b)
@@ -81,7 +88,7 @@ def check(key, a, base_perm):
     dv.check_hang()
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c3t", "c4"])
 def test_config_bitwise(cfg):
     a, base, _ = W.config_matrix(cfg)
     if base == "rcm":
@@ -96,3 +103,40 @@ def test_config_bitwise(cfg):
 @pytest.mark.parametrize("seed", [0, 1])
 def test_rmat_bitwise(seed):
     check(f"c5_seed{seed}", W.rmat(18, seed), None)
+
+
+def test_rmat_batch_all_seeds():
+    """The whole c5 batch (64 R-MAT systems, one block-diagonal plan as in
+    bench.py): every system's factor values and solution bitwise equal to
+    the reference's own run of that seed."""
+    seeds = [s for s in range(64) if f"c5_seed{s}" in DIGESTS]
+    assert len(seeds) == 64
+    mats = [W.rmat(18, s) for s in seeds]
+    sizes = [m.n for m in mats]
+    a = W.block_diagonal(mats)
+    del mats
+    plan = build_plan(a, k=0, tau=0.0, min_level_rows=16)
+    ilu = plan.ilu
+    n = a.n
+    assert ilu.factor() == -1
+    perm = dv.host_i64(plan.perm, n)
+    b = np.concatenate([np.random.default_rng(0).uniform(-1.0, 1.0, m) for m in sizes])[perm]
+    bd = dv.f64(b)
+    y = dv.empty_f64(n)
+    x = dv.empty_f64(n)
+    ilu.solve_async(0, bd, y)
+    ilu.solve_async(1, y, x)
+    rs = dv.host_i64(ilu.row_start, n + 1)
+    val = ilu.host_val()
+    xh = dv.host_f64(x, n)
+    off = 0
+    for s, m in zip(seeds, sizes):
+        rows = np.flatnonzero((perm >= off) & (perm < off + m))
+        off += m
+        lens = rs[rows + 1] - rs[rows]
+        starts = np.concatenate([[0], np.cumsum(lens)])[:-1]
+        idx = np.repeat(rs[rows] - starts, lens) + np.arange(int(lens.sum()))
+        d = DIGESTS[f"c5_seed{s}"]["digests"]
+        assert h(val[idx], "f") == d["fval"], s
+        assert h(xh[rows], "f") == d["x"], s
+    dv.check_hang()

@@ -4,6 +4,8 @@ reference's krylov.py in oracle/ (iteration counts, solutions) and the
 reference's own behavioural cases (exact preconditioners, zero RHS,
 breakdown, Krylov optimality, ordering experiment)."""
 
+import json
+
 import numpy as np
 import pytest
 
@@ -129,3 +131,62 @@ def test_iteration_experiment_orderings():
     un = jv.convdiff2d(10, seed=2)
     rows = jv.iteration_experiment(un, orderings=[("natural", None, False)])
     assert rows[0]["method"] == "gmres" and rows[0]["converged"]
+
+
+# ---- pinned to the reference's own krylov.py runs (tests/golden/krylov.npz)
+
+from test_krylov_golden import NAMES as KNAMES, Z as KZ, case as kcase  # noqa: E402
+
+
+@pytest.mark.parametrize("precond_kind", ["device", "reference_lambda"])
+@pytest.mark.parametrize("name", KNAMES)
+def test_krylov_matches_reference_fixture(name, precond_kind):
+    """Iteration counts equal to the reference's; residual histories and
+    solutions within 1e-7 relative.  "reference_lambda" drives the
+    preconditioner exactly as the reference's pipeline does
+    (`lambda r: apply_preconditioner(f, r)`, pipeline.py:300)."""
+    g = kcase(name)
+    m = g["meta"]
+    a = jv.CsrMatrix(g["a_rs"].size - 1, g["a_rs"], g["a_col"], g["a_val"])
+    pre = None
+    if m["k"] is not None:
+        f = ilu(a, m["k"])
+        pre = (jv.ilu_preconditioner(f) if precond_kind == "device"
+               else (lambda r: jv.apply_preconditioner(f, r)))
+    elif precond_kind != "device":
+        pytest.skip("unpreconditioned case runs once")
+    if m["method"] == "pcg":
+        res = jv.pcg(a, g["b"], pre, tol=m["tol"], maxit=m["maxit"])
+    else:
+        res = jv.gmres(a, g["b"], pre, restart=m["restart"], tol=m["tol"], maxit=m["maxit"])
+    assert res.iterations == int(g["iterations"]) and res.converged == bool(g["converged"])
+    assert np.allclose(res.residual_history, g["history"], rtol=1e-7, atol=1e-14)
+    assert np.allclose(res.x, g["x"], rtol=1e-7, atol=1e-10)
+
+
+def test_criterion_7_on_device():
+    """Acceptance criterion 7 (test_acceptance.py:245-261): Poisson 64x64,
+    tol 1e-6 -> ILU(0)-PCG 43 iterations < plain CG 104."""
+    a = jv.poisson2d(64)
+    b = jv.spmv(a, np.ones(a.n))
+    plain = jv.pcg(a, b, tol=1e-6, maxit=2000)
+    f = ilu(a)
+    pre = jv.pcg(a, b, lambda r: jv.apply_preconditioner(f, r), tol=1e-6, maxit=2000)
+    dev = jv.pcg(a, b, jv.ilu_preconditioner(f), tol=1e-6, maxit=2000)
+    assert plain.converged and plain.iterations == 104
+    assert pre.converged and pre.iterations == 43
+    assert dev.converged and dev.iterations == 43
+
+
+def test_iteration_experiment_matches_reference_rows():
+    exp = json.loads(str(KZ["_experiment"][0]))
+    a = jv.poisson2d(12)
+    rcm = jv.Permutation(KZ["_experiment_rcm12"])
+    assert np.array_equal(jv.rcm_order(a.pattern).perm, rcm.perm)
+    rows = jv.iteration_experiment(
+        a, orderings=[("NAT", None, False), ("RCM", rcm, False), ("LS-RCM", rcm, True),
+                      ("LS-NAT", None, True)], tol=1e-6)
+    assert rows == exp["poisson12"]
+    cd = jv.convdiff2d(8, seed=3)
+    rows = jv.iteration_experiment(cd, orderings=[("NAT", None, False), ("LS-NAT", None, True)])
+    assert rows == exp["convdiff8"]
