@@ -20,6 +20,7 @@ oracle, threaded point-to-point version) on the host cores.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import hashlib
 import json
 import os
@@ -144,11 +145,38 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _median_runs(fn, budget_s, max_runs=5, prep=None):
+    """Median wall time of fn() over up to max_runs runs within budget_s
+    (at least one); prep() runs untimed before each."""
+    ts = []
+    deadline = time.perf_counter() + budget_s
+    while len(ts) < max_runs and (not ts or time.perf_counter() < deadline):
+        if prep is not None:
+            prep()
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), len(ts)
+
+
 def cpu_baseline(cfg, plan, seconds=12.0, blocks=None):
-    """The reference's algorithm on the host (the pinned C oracle), serial
-    and threaded, on the same matrix; bounded to ~`seconds` of CPU work.
+    """The reference's algorithms on the host (the pinned C oracle) on the
+    same matrix: factor (serial 1 core; point-to-point threads on all
+    cores), stri pair (serial sweeps; p2p threaded sweeps), spmv (1 core,
+    the reference's is single-threaded).  Each path: median of up to 5 runs
+    within its share of `seconds`; value copies made outside the timing.
     For the c5 batch the sample is ONE system of the batch (the throughput
-    unit, nnz/s, is per-nonzero so it carries over)."""
+    units are per nonzero / per byte, so they carry over)."""
     import oracle
     from paper_1812_06160_b200 import device as dv
 
@@ -158,33 +186,56 @@ def cpu_baseline(cfg, plan, seconds=12.0, blocks=None):
     col = dv.host_i64(ilu.col, ilu.nnz)
     diag = dv.host_i64(ilu.diag_pos, n)
     val = dv.host_f64(plan.assembled, ilu.nnz)
-    sample = f"full {cfg} factorization"
+    prs, pcol = plan.permuted.host_pattern()
+    pval = dv.host_f64(plan.permuted.val, plan.permuted.nnz)
+    sample = f"full {cfg} matrix"
     if blocks is not None:
         from paper_1812_06160_b200 import workloads as W
         sd = blocks[0][0]
-        fe = oracle.front_end(*(lambda m: (m.n, m.row_start, m.col, m.val))(W.rmat(18, sd)))
+        m = W.rmat(18, sd)
+        fe = oracle.front_end(m.n, m.row_start, m.col, m.val)
         rs, col, diag, val = fe["row_start"], fe["col"], fe["diag"], fe["val"]
+        prs, pcol, pval = fe["permuted"]
+        n = m.n
         sample = f"one system of the c5 batch (R-MAT seed {sd})"
     tau = ilu.tau
     cores = os.cpu_count() or 1
-    res = {}
-    deadline = time.perf_counter() + seconds
-    ts, tp = [], []
-    while time.perf_counter() < deadline or len(ts) < 1:
-        t0 = time.perf_counter()
-        oracle.factor_serial(rs, col, val, diag, tau)
-        ts.append(time.perf_counter() - t0)
-        t0 = time.perf_counter()
-        oracle.p2p(0, cores, rs, col, val, diag, tau)
-        tp.append(time.perf_counter() - t0)
-        if len(ts) >= 5:
-            break
-    res["serial_s"] = statistics.median(ts)
-    res["threaded_s"] = statistics.median(tp)
-    res["runs"] = len(ts)
-    res["nnz"] = int(col.size)
-    res["sample"] = f"{sample}, serial + threaded p2p oracle x{len(ts)}"
-    return res, cores
+    nnz_f, nnz_a = int(col.size), int(pcol.size)
+    ab = alg_bytes(n, nnz_a, nnz_f)
+    share = seconds / 5.0
+    v = np.empty_like(val)
+    refresh = lambda: np.copyto(v, val)
+    fs, k1 = _median_runs(lambda: oracle.p2p(0, 1, rs, col, v, diag, tau, inplace=True), share,
+                          prep=refresh)
+    ft, k2 = _median_runs(lambda: oracle.p2p(0, cores, rs, col, v, diag, tau, inplace=True), share,
+                          prep=refresh)
+    fval, _ = oracle.factor_serial(rs, col, val, diag, tau)
+    b = np.random.default_rng(0).uniform(-1.0, 1.0, n)
+    ss, k3 = _median_runs(lambda: oracle.solve_backward(
+        rs, col, fval, diag, oracle.solve_forward(rs, col, fval, b)), share)
+    x = np.empty(n)
+
+    def thr():
+        np.copyto(x, b)
+        oracle.p2p(1, cores, rs, col, fval, diag, vec=x, inplace=True)
+        oracle.p2p(2, cores, rs, col, fval, diag, vec=x, inplace=True)
+    st, k4 = _median_runs(thr, share)
+    sp, k5 = _median_runs(lambda: oracle.spmv(prs, pcol, pval, b), share)
+    GB = lambda nb, t: nb / t / 1e9
+    return {
+        "value": nnz_f / ft, "unit": "factor nnz/s", "cores": cores, "kind": "port",
+        "sample": f"{sample}; pinned C restatement of the reference kernels; medians of "
+                  f"{min(k1, k2, k3, k4, k5)}-5 runs",
+        "serial_value": nnz_f / fs, "serial_cores": 1, "cpu_model": cpu_model(),
+        "paths": {
+            "factor": {"serial_ms": fs * 1e3, "threaded_ms": ft * 1e3, "threads": cores,
+                       "serial_nnz_per_s": nnz_f / fs, "threaded_nnz_per_s": nnz_f / ft},
+            "stri": {"serial_ms": ss * 1e3, "threaded_ms": st * 1e3, "threads": cores,
+                     "serial_GBps": GB(ab["stri"], ss), "threaded_GBps": GB(ab["stri"], st),
+                     "sweeps": "forward+backward (serial = solve_serial; threaded = solve_ls p2p)"},
+            "spmv": {"serial_ms": sp * 1e3, "GBps": GB(ab["spmv"], sp), "threads": 1},
+        },
+    }
 
 
 def digest(a, kind):
@@ -446,9 +497,44 @@ def run_mine(args):
     peak, peak_kind = peaks()
     # per-GPU algorithmic bytes (every rank factors its own matrix / shard)
     ach = ab["factor"] / f_avg / 1e9
-    prof = load_profile(args.config)
-    impl = {sw: ("region" if ilu._region_for(sw) is not None else "tickets")
-            for sw in ("factor", "fwd", "bwd")}
+    prof = load_profile(args.config) or {}
+
+    def impl_of(sw):
+        rp = ilu._region_for(sw)
+        return "tickets" if rp is None else ("two_stage" if rp is dv.TWO_STAGE else "region")
+    impl = {sw: impl_of(sw) for sw in ("factor", "fwd", "bwd")}
+
+    # DAG depths and the measured cross-SM hop: depth x t_hop is the floor of
+    # a sweep whose consecutive levels sit on different SMs
+    hop_ns = ctypes.c_double(0.0)
+    _L.call("jv_hop_latency", 20000, ctypes.byref(hop_ns))
+    t_hop_us = hop_ns.value / 1e3
+    fdepth = dv.levels_dev(ilu.pattern, False)[1]
+    bdepth = dv.levels_dev(ilu.pattern, True)[1]
+    tail = measure_tail(ilu, plan, K) if plan.n_upper < n else None
+
+    def roof(nbytes, secs, depth, kernel, traffic_key):
+        a = nbytes / secs / 1e9
+        return {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak,
+                "peak_kind": peak_kind, "alg_bytes": nbytes, "us": secs * 1e6,
+                "traffic": prof.get(traffic_key), "kernel": kernel, "dag_depth": depth,
+                "t_hop_us": t_hop_us, "depth_x_thop_us": depth * t_hop_us}
+    rooflines = {
+        "factor": roof(ab["factor"], f_avg, fdepth,
+                       {"tickets": "factor_kernel", "region": "region_kernel<0>",
+                        "two_stage": "factor_kernel + tail_upper_kernel"}[impl["factor"]],
+                       "factor_dram_bytes"),
+        "stri": roof(ab["stri"], st_avg, fdepth + bdepth,
+                     f"fwd {impl['fwd']} + bwd {impl['bwd']}", "stri_dram_bytes"),
+        "spmv": roof(ab["spmv"], sp_avg, 0, "spmv_stream_kernel", "spmv_dram_bytes"),
+    }
+    if tail is not None:
+        tail_nnz = int(dv.host_i64(ilu.row_start[plan.n_upper:], 1)[0])
+        tb = 20 * (nnz_f - tail_nnz) + 8 * (n - plan.n_upper) + 4
+        tail["stage1_roofline"] = roof(tb, tail["stage1_us"] / 1e6, 0, "tail_upper_kernel",
+                                       "tail_dram_bytes")
+        tail["stage1_roofline"]["note"] = ("alg bytes = the tail rows' share of the factor "
+                                           "formula (20 nnz_tail + 8 n_tail + 4)")
     paths = {
         "impl": impl, "autotune_ms": {k: list(v) for k, v in ilu.autotune_ms.items()},
         "factor": {"us": f_avg * 1e6, "nnz_per_s": nnz_f / f_avg, "alg_bytes": ab["factor"],
@@ -457,6 +543,7 @@ def run_mine(args):
                  "frac": ab["stri"] / st_avg / 1e9 / peak,
                  "fwd_us": sum(fw_ms) / K * 1e3, "bwd_us": sum(bw_ms) / K * 1e3},
         "stri_csrls_baseline": csrls,
+        "tail": tail,
         "spmv": {"us": sp_avg * 1e6, "alg_bytes": ab["spmv"], "GBps": ab["spmv"] / sp_avg / 1e9,
                  "frac": ab["spmv"] / sp_avg / 1e9 / peak},
     }
@@ -487,10 +574,8 @@ def run_mine(args):
                    "total_nnz_f": tot_nnz_f, "k": s["k"], "tau": s["tau"], "levels": plan.nlev,
                    "n_upper": plan.n_upper, "parallelism": par,
                    "l2": "inputs > 126 MB L2, no flush needed"},
-        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": ach / peak, "peak_kind": peak_kind,
-                     "traffic": prof.get("factor_dram_bytes") if prof else None,
-                     "kernel": "factor_kernel" if impl["factor"] == "tickets" else "region_kernel<0>"},
+        "roofline": dict(rooflines["factor"]),
+        "rooflines": rooflines,
         "paths": paths,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -502,16 +587,48 @@ def run_mine(args):
     if multi:
         line["multi_gpu"] = multi
     if world == 1 and rank == 0 and not args.no_cpu:
-        cb, cores = cpu_baseline(args.config, plan, seconds=args.cpu_seconds, blocks=blocks)
-        line["cpu_baseline"] = {
-            "value": cb["nnz"] / cb["threaded_s"], "unit": "factor nnz/s", "cores": cores,
-            "kind": "port", "sample": cb["sample"],
-            "serial_value": cb["nnz"] / cb["serial_s"], "serial_cores": 1,
-        }
+        cb = cpu_baseline(args.config, plan, seconds=args.cpu_seconds, blocks=blocks)
+        cp = cb["paths"]
+        cp["factor"]["gpu_speedup_vs_threaded"] = (nnz_f / f_avg) / cb["value"]
+        cp["stri"]["gpu_speedup_vs_threaded"] = cp["stri"]["threaded_ms"] / 1e3 / st_avg
+        cp["spmv"]["gpu_speedup_vs_serial"] = cp["spmv"]["serial_ms"] / 1e3 / sp_avg
+        line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_tail(ilu, plan, K):
+    """The two-stage path timed on its own, whatever the
+    autotune picked for the step: upper rows, then the segmented tail
+    stage 1 and the corner, CUDA events on the stream; bitwise check
+    against the step's factor values."""
+    import torch
+    from paper_1812_06160_b200 import device as dv
+
+    want = ilu.val.clone()
+    n_upper = plan.n_upper
+    tp = ilu.tail_plan(n_upper)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    up, s1, cr = [], [], []
+    for k in range(K + 2):
+        plan.reset_values()
+        ev[0].record()
+        ilu.factor_two_stage_async(n_upper, ev=ev[1:])
+        torch.cuda.synchronize()
+        if k >= 2:
+            up.append(ev[0].elapsed_time(ev[1]) * 1e3)
+            s1.append(ev[1].elapsed_time(ev[2]) * 1e3)
+            cr.append(ev[2].elapsed_time(ev[3]) * 1e3)
+    same = bool(torch.equal(ilu.val, want))
+    dv.check_hang()
+    return {"n_upper": n_upper, "tail_rows": tp.nt, "corner_entries": tp.nc,
+            "stage1_updates": tp.nops, "stage1_groups": tp.ngroups, "stage1_segments": tp.nsegs,
+            "upper_us": statistics.median(up), "stage1_us": statistics.median(s1),
+            "corner_us": statistics.median(cr),
+            "two_stage_us": statistics.median(up) + statistics.median(s1) + statistics.median(cr),
+            "bitwise_equal_to_step": same}
 
 
 def measure_e2e(a, plan, args):
@@ -579,28 +696,32 @@ def run_reference(args):
     rs, col, diag, val = fe["row_start"], fe["col"], fe["diag"], fe["val"]
     nnz_f = col.size
     cores = os.cpu_count() or 1
+    v = np.empty_like(val)
     for _ in range(args.warmup):
-        oracle.p2p(0, cores, rs, col, val, diag, s["tau"])
+        np.copyto(v, val)
+        oracle.p2p(0, cores, rs, col, v, diag, s["tau"], inplace=True)
     ts = []
     for _ in range(args.steps):
+        np.copyto(v, val)      # the refresh is not part of the factorization
         t0 = time.perf_counter()
-        oracle.p2p(0, cores, rs, col, val, diag, s["tau"])
+        oracle.p2p(0, cores, rs, col, v, diag, s["tau"], inplace=True)
         ts.append(time.perf_counter() - t0)
     t = sum(ts) / len(ts)
-    v = nnz_f / t
+    rate = nnz_f / t
     print(json.dumps({
         "impl": "reference",
         "metric": "ILU factor nnz/s, stri and spmv GB/s (fp64) vs HBM roofline; 1/2/4/8 GPU",
-        "value": v, "unit": "factor nnz/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "value": rate, "unit": "factor nnz/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY.md §8d recipe)",
         "config": {"workload": f"{args.config}:{s['name']}", "n": a.n, "nnz_f": nnz_f},
-        "cpu_baseline": {"value": v, "unit": "factor nnz/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": rate, "unit": "factor nnz/s", "cores": cores, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": (f"one R-MAT system of the c5 batch per step" if args.config == "c5"
                                     else f"full {args.config} factorization per step") +
                                    ", threaded p2p restatement of factor_p2p_kernel"},
-        "e2e": {"value": v, "unit": "factor nnz/s", "h2d_bytes_per_step": 0,
+        "e2e": {"value": rate, "unit": "factor nnz/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))
 

@@ -381,6 +381,10 @@ int jv_tail_upper(int64_t handle, const int32_t* col, const int32_t* diag_pos, d
 int jv_tail_corner(int64_t handle, int32_t* row_start, int32_t* col, int32_t* diag_pos,
                    int32_t* pos, void* stream);
 int jv_tail_plan_free(int64_t handle);
+/* latency of one dependent cross-SM mailbox hop (ns), measured by a chain of
+ * `hops` steps on consecutive SMs (synchronous; diagnostics for the bench's
+ * depth x t_hop bound) */
+int jv_hop_latency(int32_t hops, double* ns_per_hop_h);
 int jv_scatter(int64_t n, const int32_t* idx, const double* src, double* dst, void* stream);
 
 #ifdef __cplusplus

@@ -94,6 +94,7 @@ _SIGS = {
     "jv_tail_corner": [c_int64, _P, _P, _P, _P, _P],
     "jv_tail_plan_free": [c_int64],
     "jv_scatter": [c_int64, _P, _P, _P, _P],
+    "jv_hop_latency": [c_int32, POINTER(c_double)],
 }
 _RESTYPES = {
     "jv_last_error": ctypes.c_char_p,

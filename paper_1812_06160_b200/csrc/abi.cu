@@ -214,3 +214,48 @@ extern "C" int jv_test_ddiv(int32_t n, const double* a, const double* b, double*
   JV_CHECK_LAUNCH("jv_test_ddiv");
   return JV_OK;
 }
+
+// ---- t_hop: latency of one dependent cross-SM hop through a mailbox packet
+// (the primitive every sync-free kernel waits on).  A chain of K steps, step
+// k owned by CTA k mod grid (one warp per CTA, consecutive steps on
+// different SMs): step k polls step k-1's packet, adds one, publishes.
+// Kernel time / K = t_hop, the per-level floor of a DAG sweep whose
+// consecutive levels live on different SMs (SURVEY.md §8d "depth bound").
+namespace {
+__global__ void hop_chain_kernel(int K, uint64_t* box, uint32_t epoch) {
+  if (threadIdx.x != 0) return;
+  for (int k = blockIdx.x; k < K; k += gridDim.x) {
+    double v = 0.0;
+    if (k > 0) {
+      while (!jv::mbox_try(box, k - 1, epoch, v)) {
+      }
+    }
+    jv::mbox_put(box, k, v + 1.0, epoch);
+  }
+}
+}  // namespace
+
+extern "C" int jv_hop_latency(int32_t hops, double* ns_per_hop_h) {
+  if (hops < 2 || !ns_per_hop_h) { jvh::set_error("jv_hop_latency: bad args"); return JV_EINVAL; }
+  uint64_t* box = nullptr;
+  cudaError_t e = cudaMalloc(&box, 16 * (size_t)hops);
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_hop_latency");
+  cudaMemset(box, 0, 16 * (size_t)hops);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = jvh::sm_count();
+  hop_chain_kernel<<<grid, 32>>>(hops, box, 1u);   // warm-up
+  cudaEventRecord(a);
+  hop_chain_kernel<<<grid, 32>>>(hops, box, 2u);
+  cudaEventRecord(b);
+  e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(box);
+  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_hop_latency");
+  *ns_per_hop_h = (double)ms * 1e6 / hops;
+  return JV_OK;
+}

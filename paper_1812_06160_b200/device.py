@@ -124,6 +124,14 @@ def _registered(a):
     return True
 
 
+STREAM_MIN_BYTES = 32 << 20    # streamed factor_serial above this many value bytes
+
+
+def pinned_host(a):
+    """Page-lock a float64 host array in place when possible (True if so)."""
+    return isinstance(a, np.ndarray) and a.dtype == np.float64 and _registered(a)
+
+
 def upload_f64(dst, src):
     """dst (device tensor) <- src (host float64 numpy array)."""
     t = torch()
@@ -856,18 +864,21 @@ class DevIlu:
             self.compute_norms()
         self._region_run(rp, 0, None, None, self.fbox, reset=self.err)
 
-    def _factor_tickets(self, lo, hi, ready_below, norms):
+    def _factor_tickets(self, lo, hi, ready_below, norms, reset=True):
         sched = self.factor_schedule()
         el = self.elim_lists()
         hub = self.hub_plans()
         if lo > 0 or hi < self.n:
-            key = (lo, hi, id(sched))
-            if getattr(self, "_sub", None) is None or self._sub[0] != key:
-                self._sub = (key, sched.restrict(lo, hi))
-            sched = self._sub[1]
+            if getattr(self, "_sub", None) is None or self._sub[0] is not sched:
+                self._sub = (sched, {})
+            key = (lo, hi)
+            if key not in self._sub[1]:
+                self._sub[1][key] = sched.restrict(lo, hi)
+            sched = self._sub[1][key]
         if norms:
             self.compute_norms()
-        _lib.call("jv_reset_row", ptr(self.err), stream())
+        if reset:
+            _lib.call("jv_reset_row", ptr(self.err), stream())
         _lib.call("jv_factor", self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
                   ptr(self.diag_pos), ptr(self.norms), self.tau, int(self.milu), ptr(sched.order),
                   ptr(sched.batch_ptr), sched.nbatch, int(ready_below), ptr(self.fbox.buf),
@@ -886,7 +897,7 @@ class DevIlu:
             self._tail = (key, TailPlan(self, int(n_upper)))
         return self._tail[1]
 
-    def factor_tail_async(self, n_upper, norms=True):
+    def factor_tail_async(self, n_upper, norms=True, ev=None):
         """Two-stage lower tail (lower.py:273-318): stage 1 eliminates every
         tail row's upper-stage pivots (jv_tail_upper, segmented, one warp
         per row), stage 2 factors the corner with the sync-free kernel on
@@ -897,8 +908,12 @@ class DevIlu:
             return tp
         if norms and self.tau > 0:
             self.compute_norms()
+        if ev is not None:
+            ev[0].record()
         _lib.call("jv_tail_upper", tp.h, ptr(self.col), ptr(self.diag_pos), ptr(self.val),
                   ptr(self.norms), self.tau, stream())
+        if ev is not None:
+            ev[1].record()
         c = tp.corner
         if tp.nc:
             _lib.call("jv_gather", tp.nc, ptr(tp.pos), ptr(self.val), ptr(c.val), stream())
@@ -910,6 +925,8 @@ class DevIlu:
         c._factor_tickets(0, tp.nt, 0, False)
         if tp.nc:
             _lib.call("jv_scatter", tp.nc, ptr(tp.pos), ptr(c.val), ptr(self.val), stream())
+        if ev is not None:
+            ev[2].record()
         self.values_changed()
         return tp
 
@@ -931,12 +948,102 @@ class DevIlu:
         self.values_changed()
         return n_upper + bad
 
-    def factor_two_stage_async(self, n_upper):
-        """Upper rows with the sync-free kernel, then the lower tail."""
+    def factor_two_stage_async(self, n_upper, ev=None):
+        """Upper rows with the sync-free kernel, then the lower tail
+        (ev: 3 events recorded before stage 1, after it, after the corner)."""
         if n_upper > 0:
             self._factor_tickets(0, n_upper, 0, True)
-        self.factor_tail_async(n_upper, norms=(n_upper == 0))
+        self.factor_tail_async(n_upper, norms=(n_upper == 0), ev=ev)
         self.values_changed()
+
+    # streamed drop-in factorization: host values in, factors out -------
+    STREAM_CHUNKS = 8
+
+    STREAM_ENDS = 2       # small chunks at each end (pipeline fill and drain)
+
+    def _chunks(self, k):
+        """Row bounds of k chunks balanced by stored entries, plus
+        STREAM_ENDS chunks of a quarter size at both ends, so the pipeline
+        fills and drains quickly (cached)."""
+        key = ("chunks", k, self.STREAM_ENDS)
+        if getattr(self, "_chunk_cache", None) is None or self._chunk_cache[0] != key:
+            rs = self._host_pattern()[0].astype(np.int64)
+            e = 1.0 / (4 * k)
+            ends = [e * i for i in range(1, self.STREAM_ENDS + 1)]
+            inner = np.linspace(ends[-1] if ends else 0.0, 1.0 - (ends[-1] if ends else 0.0),
+                                k + 1)
+            fr = np.unique(np.concatenate([[0.0], ends, inner, [1.0 - x for x in ends], [1.0]]))
+            tgt = fr * self.nnz
+            b = np.unique(np.searchsorted(rs, tgt, side="left").clip(0, self.n))
+            b[0], b[-1] = 0, self.n
+            self._chunk_cache = (key, b, rs)
+        return self._chunk_cache[1], self._chunk_cache[2]
+
+    def factor_streamed(self, host_val):
+        """factor_serial with host values (a page-locked float64 array, read
+        and overwritten in place): the rows are cut into chunks in level
+        order; chunk c's upload, chunk c-1's factorization (sync-free kernel
+        over those rows, earlier rows final) and chunk c-2's download run
+        concurrently on three streams, so the host link in both directions
+        overlaps the device work.  Returns the smallest zero-pivot row or -1;
+        rows after it get their input values back (the reference stops
+        there)."""
+        t = torch()
+        main = t.cuda.current_stream()
+        if getattr(self, "_xfer", None) is None:
+            self._xfer = (t.cuda.Stream(), t.cuda.Stream())
+            self._vbak = None
+        s_in, s_out = self._xfer
+        if self._vbak is None or self._vbak.numel() < self.nnz:
+            self._vbak = empty_f64(self.nnz)
+        bounds, rs = self._chunks(self.STREAM_CHUNKS)
+        hp = host_val.ctypes.data
+        dp = self.val.data_ptr()
+        s_in.wait_stream(main)
+        _lib.call("jv_reset_row", ptr(self.err), stream())
+        done_in, done_f = [], []
+        for c in range(bounds.size - 1):
+            lo, hi = int(bounds[c]), int(bounds[c + 1])
+            p0, p1 = int(rs[lo]), int(rs[hi])
+            if p1 > p0:
+                _lib.call("jv_memcpy_async", ctypes.c_void_p(dp + 8 * p0),
+                          ctypes.c_void_p(hp + 8 * p0), 8 * (p1 - p0), 0,
+                          ctypes.c_void_p(s_in.cuda_stream))
+            e = t.cuda.Event()
+            e.record(s_in)
+            done_in.append(e)
+        for c in range(bounds.size - 1):
+            lo, hi = int(bounds[c]), int(bounds[c + 1])
+            p0, p1 = int(rs[lo]), int(rs[hi])
+            main.wait_event(done_in[c])
+            self._vbak[p0:p1].copy_(self.val[p0:p1])
+            if self.tau > 0 and hi > lo:
+                _lib.call("jv_row_norms", hi - lo, ctypes.c_void_p(self.row_start.data_ptr() + 4 * lo),
+                          ptr(self.val), self.tau, ctypes.c_void_p(self.norms.data_ptr() + 8 * lo),
+                          stream())
+            if hi > lo:
+                self._factor_tickets(lo, hi, lo, False, reset=False)
+            e = t.cuda.Event()
+            e.record(main)
+            done_f.append(e)
+            s_out.wait_event(e)
+            if p1 > p0:
+                _lib.call("jv_memcpy_async", ctypes.c_void_p(hp + 8 * p0),
+                          ctypes.c_void_p(dp + 8 * p0), 8 * (p1 - p0), 1,
+                          ctypes.c_void_p(s_out.cuda_stream))
+        main.wait_stream(s_out)
+        self.values_changed()
+        bad = read_row_slot(self.err)
+        check_hang()
+        if bad >= 0:
+            p = int(rs[bad + 1])
+            if p < self.nnz:
+                _lib.call("jv_memcpy_async", ctypes.c_void_p(hp + 8 * p),
+                          ctypes.c_void_p(self._vbak.data_ptr() + 8 * p), 8 * (self.nnz - p), 1,
+                          stream())
+                self.val[p:self.nnz].copy_(self._vbak[p:self.nnz])
+            sync()
+        return bad
 
     def factor(self, lo=0, hi=None, ready_below=0):
         """Factor and return the smallest zero-pivot row (or -1)."""

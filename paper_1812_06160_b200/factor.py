@@ -51,7 +51,15 @@ def factor_serial(factors: IluFactors) -> None:
     matches the reference's."""
     if factors.n == 0:
         return
-    bad = _run(factors, keep_after_bad=True)
+    factors.val = np.ascontiguousarray(factors.val, dtype=np.float64)
+    if factors.pattern.nnz * 8 >= dv.STREAM_MIN_BYTES and dv.pinned_host(factors.val):
+        # large page-locked host values: upload, factorization and download
+        # overlap chunk by chunk (DevIlu.factor_streamed)
+        d = factors.device()
+        bad = d.factor_streamed(factors.val)
+        d.holder = factors
+    else:
+        bad = _run(factors, keep_after_bad=True)
     if bad >= 0:
         raise ZeroPivotError(int(bad))
 
