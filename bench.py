@@ -55,23 +55,21 @@ def alg_bytes(n, nnz_a, nnz_f):
     )
 
 
-def build_config(cfg, rank=0, world=1, rmat_count=64):
+def build_config(cfg, rank=0, world=1, rmat_count=64, first=0):
     """Matrix + device plan of the config.  c5 (a batch of independent R-MAT
-    systems) is sharded: this rank builds the block-diagonal matrix of its
-    contiguous block of seeds (dist.shard_range); `blocks` lists them."""
+    systems) is sharded (dist.BatchShard): this rank builds the
+    block-diagonal matrix of its contiguous block of seeds; `blocks` is the
+    shard."""
     import paper_1812_06160_b200 as jv
     from paper_1812_06160_b200 import workloads as W
-    from paper_1812_06160_b200.dist import shard_range
+    from paper_1812_06160_b200.dist import BatchShard
     from paper_1812_06160_b200.plan import build_plan
 
     blocks = None
     if cfg == "c5":
         s = W.CONFIGS[cfg]
-        seeds = list(shard_range(rmat_count, rank, world))
-        mats = [W.rmat(18, sd) for sd in seeds]
-        blocks = [(sd, m.n) for sd, m in zip(seeds, mats)]
-        a, base = W.block_diagonal(mats), None
-        del mats
+        blocks = BatchShard(rmat_count, rank, world, first)
+        a, base = blocks.assemble(lambda sd: W.rmat(18, sd)), None
     else:
         a, base, s = W.config_matrix(cfg)
     if base == "rcm":
@@ -90,7 +88,7 @@ def rhs(n, blocks):
     the reference's krylov.py:199 / SURVEY.md §8d), one draw per block."""
     if blocks is None:
         return np.random.default_rng(0).uniform(-1.0, 1.0, n)
-    return np.concatenate([np.random.default_rng(0).uniform(-1.0, 1.0, m) for _, m in blocks])
+    return np.concatenate([np.random.default_rng(0).uniform(-1.0, 1.0, m) for m in blocks.sizes])
 
 
 class ClockSampler:
@@ -191,7 +189,7 @@ def cpu_baseline(cfg, plan, seconds=12.0, blocks=None):
     sample = f"full {cfg} matrix"
     if blocks is not None:
         from paper_1812_06160_b200 import workloads as W
-        sd = blocks[0][0]
+        sd = blocks.seeds[0]
         m = W.rmat(18, sd)
         fe = oracle.front_end(m.n, m.row_start, m.col, m.val)
         rs, col, diag, val = fe["row_start"], fe["col"], fe["diag"], fe["val"]
@@ -243,24 +241,6 @@ def digest(a, kind):
     return hashlib.sha256(a.tobytes()).hexdigest()
 
 
-def block_rows(perm, blocks):
-    """New-order rows of each block of a block-diagonal plan (c5): the level
-    permutation keeps every block's relative order, so these rows, in order,
-    are exactly that system's own factor rows."""
-    out, off = {}, 0
-    for sd, m in blocks:
-        out[sd] = np.flatnonzero((perm >= off) & (perm < off + m))
-        off += m
-    return out
-
-
-def take_rows(rs, val, rows):
-    lens = rs[rows + 1] - rs[rows]
-    starts = np.concatenate([[0], np.cumsum(lens)])[:-1]
-    idx = np.repeat(rs[rows] - starts, lens) + np.arange(int(lens.sum()))
-    return val[idx]
-
-
 def parity_check(cfg, ilu, plan, x, sy, blocks, n):
     """Bitwise digests of the timed arrays against the reference's full-size
     digests (tests/golden/full_digests.json); None when none apply."""
@@ -276,11 +256,12 @@ def parity_check(cfg, ilu, plan, x, sy, blocks, n):
         return (digest(ilu.host_val(), "f") == d["digests"]["fval"]
                 and digest(dv.host_f64(x, n), "f") == d["digests"]["x"]
                 and digest(dv.host_f64(sy, n), "f") == d["digests"]["spmv_perm"])
-    have = [sd for sd, _ in blocks if f"c5_seed{sd}" in allg]
+    have = [sd for sd in blocks.seeds if f"c5_seed{sd}" in allg]
+    parity_check.detail = {"systems_checked": len(have), "systems": len(blocks.seeds)}
     if not have:
         return None
     perm = dv.host_i64(plan.perm, n)
-    rows = block_rows(perm, blocks)
+    rows = blocks.system_rows(perm)
     rs = dv.host_i64(ilu.row_start, n + 1)
     val = ilu.host_val()
     xh, syh = dv.host_f64(x, n), dv.host_f64(sy, n)
@@ -288,11 +269,67 @@ def parity_check(cfg, ilu, plan, x, sy, blocks, n):
     for sd in have:
         d = allg[f"c5_seed{sd}"]["digests"]
         r = rows[sd]
-        ok &= digest(take_rows(rs, val, r), "f") == d["fval"]
+        ok &= digest(blocks.take_rows(rs, val, r), "f") == d["fval"]
         ok &= digest(xh[r], "f") == d["x"]
         # the block's spmv rows: hub rows beyond one tile are tree-summed
         # (1e-12), so the spmv digest is informative only
     return bool(ok)
+
+
+def measure_batch(world, rank, per_gpu, steps):
+    """Batch sharding (SURVEY §8e, config 5's systems): every rank factors
+    and solves its own `per_gpu` R-MAT systems (seeds rank*per_gpu + i) as
+    one block-diagonal matrix, no collective on the hot path; per-GPU work
+    fixed (weak scaling; at 8 GPUs x 8 systems this is the full c5 batch).
+    Device time per step is the max over ranks; every system is checked
+    bitwise against the reference's digests (all 64 seeds are pinned)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1812_06160_b200 import device as dv
+
+    a, plan, s, shard = build_config("c5", rank, world, per_gpu * world)
+    ilu = plan.ilu
+    n = ilu.n
+    perm = dv.host_i64(plan.perm, n)
+    b = dv.f64(rhs(n, shard)[perm])
+    y, x = dv.empty_f64(n), dv.empty_f64(n)
+
+    def step():
+        plan.reset_values()
+        ilu.factor_async()
+        ilu.solve_async(0, b, y)
+        ilu.solve_async(1, y, x)
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / steps, float(ilu.nnz)], dtype=torch.float64,
+                      device="cuda")
+    if world > 1:
+        dist.all_reduce(ms[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(ms[1:], op=dist.ReduceOp.SUM)
+    step_ms, nnz_all = float(ms[0]), float(ms[1])
+    ok = parity_check("c5", ilu, plan, x, y, shard, n)
+    det = dict(getattr(parity_check, "detail", {}))
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, (ok, det))
+        ok = all(p[0] in (None, True) for p in parts) and any(p[0] is not None for p in parts)
+        det = {"systems_checked": sum(p[1].get("systems_checked", 0) for p in parts),
+               "systems": sum(p[1].get("systems", 0) for p in parts)}
+    dv.check_hang()
+    del plan, ilu
+    return {"systems_per_gpu": per_gpu, "systems_total": per_gpu * world, "scaling": "weak",
+            "step": "refresh + factor + forward + backward stri",
+            "step_ms_max_over_ranks": step_ms, "factor_nnz_total": nnz_all,
+            "nnz_per_s_aggregate": nnz_all / (step_ms / 1e3),
+            "bitwise_vs_reference": ok, **det}
 
 
 def measure_spmv_dist(plan, steps, world, rank):
@@ -488,11 +525,17 @@ def run_mine(args):
         e2e["value"] = (tot_nnz_f if batched else world * nnz_f) / (e2e["ms"] / 1e3)
 
     multi = None
-    if world > 1 and not batched:
+    if not batched and args.batch_per_gpu > 0:
+        multi = {}
+        if world > 1:
+            try:
+                multi["spmv_dist"] = measure_spmv_dist(plan, max(K, 20), world, rank)
+            except Exception as e:   # never lose the main line to the extra measurement
+                multi["spmv_dist"] = {"error": repr(e)[:200]}
         try:
-            multi = {"spmv_dist": measure_spmv_dist(plan, max(K, 20), world, rank)}
-        except Exception as e:   # never lose the main line to the extra measurement
-            multi = {"spmv_dist": {"error": repr(e)[:200]}}
+            multi["batch"] = measure_batch(world, rank, args.batch_per_gpu, 3)
+        except Exception as e:
+            multi["batch"] = {"error": repr(e)[:200]}
 
     peak, peak_kind = peaks()
     # per-GPU algorithmic bytes (every rank factors its own matrix / shard)
@@ -551,7 +594,7 @@ def run_mine(args):
         workload = f"c5:rmat18_x{args.rmat_count} (block-diagonal shard per rank)"
         value = tot_nnz_f / f_avg
         scaling = "strong"
-        par = f"batch-sharded dp{world} ({len(blocks)} systems on rank {rank})"
+        par = f"batch-sharded dp{world} ({len(blocks.seeds)} systems on rank {rank})"
     else:
         workload = f"{args.config}:{s['name']}"
         value = world * nnz_f / f_avg
@@ -582,6 +625,7 @@ def run_mine(args):
         "gpu_launch_detail": launch_detail,
         "clocks": clocks,
         "parity_vs_reference": parity,
+        "parity_detail": getattr(parity_check, "detail", None) if batched else None,
         "zero_pivot_row": bad,
     }
     if multi:
@@ -736,6 +780,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--rmat-count", type=int, default=64, help="c5 batch size")
+    ap.add_argument("--batch-per-gpu", type=int, default=4,
+                    help="R-MAT systems per GPU of the multi_gpu.batch measurement (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

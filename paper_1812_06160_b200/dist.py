@@ -30,7 +30,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["row_partition", "HaloPlan", "plan_halo", "DistSpmv", "DeviceOps", "shard_range"]
+__all__ = ["row_partition", "HaloPlan", "plan_halo", "DistSpmv", "DeviceOps", "shard_range",
+           "BatchShard"]
 
 
 def row_partition(row_start, parts: int) -> np.ndarray:
@@ -221,6 +222,13 @@ class DistSpmv:
             srs, scol, sval = _sub_csr(plan.rs, plan.col, plan.val, rows)
             self.parts.append((o.csr(srs, scol, sval), o.tensor_i32(rows)))
         self.send = [(q, o.tensor_i32(idx), idx.size, o.empty_f64(idx.size)) for q, idx in plan.send]
+        if plan.world > 1:
+            # NCCL requires the first collective on a communicator to include
+            # every rank; a rank without halo peers would otherwise never
+            # join it.  One tiny all-reduce at plan time initialises it.
+            import torch.distributed as dist
+            probe = self.x_ext.new_zeros(1)
+            dist.all_reduce(probe, group=group)
 
     def _post(self):
         import torch.distributed as dist
@@ -258,3 +266,55 @@ class DistSpmv:
             w.wait()
         self.boundary(y_local)
         return y_local
+
+
+class BatchShard:
+    """Batch sharding of independent systems (config 5):
+    rank p owns the contiguous block shard_range(count, p, world) of the
+    batch, stacks it into one block-diagonal matrix (workloads.block_diagonal)
+    and factors / solves it with no collective on the hot path; per-system
+    results are cut back out of the level-permuted storage (the level
+    permutation keeps every block's rows in their relative order) and,
+    off the hot path, gathered as records on every rank."""
+
+    def __init__(self, count: int, rank: int = 0, world: int = 1, first: int = 0):
+        self.count, self.rank, self.world, self.first = count, rank, world, first
+        self.seeds = [first + s for s in shard_range(count, rank, world)]
+        self.sizes = []
+
+    def assemble(self, make):
+        """Block-diagonal matrix of this rank's systems (`make(seed)` -> CsrMatrix)."""
+        from .workloads import block_diagonal
+        mats = [make(sd) for sd in self.seeds]
+        self.sizes = [m.n for m in mats]
+        return block_diagonal(mats)
+
+    def system_rows(self, perm):
+        """{seed: rows of that system in the level-permuted order}."""
+        perm = np.asarray(perm, dtype=np.int64)
+        out, off = {}, 0
+        for sd, m in zip(self.seeds, self.sizes):
+            out[sd] = np.flatnonzero((perm >= off) & (perm < off + m))
+            off += m
+        return out
+
+    @staticmethod
+    def take_rows(row_start, val, rows):
+        """The stored values of `rows` (in order), e.g. one system's factor."""
+        rs = np.asarray(row_start, dtype=np.int64)
+        lens = rs[rows + 1] - rs[rows]
+        starts = np.concatenate([[0], np.cumsum(lens)])[:-1]
+        idx = np.repeat(rs[rows] - starts, lens) + np.arange(int(lens.sum()))
+        return np.asarray(val)[idx]
+
+    def gather(self, records, group=None):
+        """All ranks' {seed: record} merged on every rank (off the hot path)."""
+        if self.world == 1:
+            return dict(records)
+        import torch.distributed as dist
+        parts = [None] * self.world
+        dist.all_gather_object(parts, dict(records), group=group)
+        out = {}
+        for p in parts:
+            out.update(p)
+        return out

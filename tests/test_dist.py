@@ -147,3 +147,113 @@ def test_plan_halo_all_matches_exchange():
             lcol = a.col[a.row_start[p.lo]:a.row_start[p.hi]]
             used = np.unique(lcol[(lcol >= plans[q].lo) & (lcol < plans[q].hi)])
             assert np.array_equal(used, ghosts)
+
+
+def _blockdiag_worker(rank, world, port, q):
+    """Every rank owns exactly one diagonal block: no halo peers at all."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = W.block_diagonal([W.laplace7(5) for _ in range(world)])
+        bounds = jd.row_partition(a.row_start, world)
+        plan = jd.plan_halo(a.row_start, a.col, a.val, bounds, rank, world)
+        sp = jd.DistSpmv(plan, NumpyOps())
+        x = np.random.default_rng(1).uniform(-1, 1, a.n)
+        y = torch.zeros(plan.n_local, dtype=torch.float64)
+        sp.x_local.copy_(torch.from_numpy(x[plan.lo:plan.hi]))
+        sp(sp.x_local, y)
+        q.put((rank, plan.lo, plan.hi, y.numpy().copy(), plan.stats))
+    except Exception as e:
+        q.put((rank, "error", repr(e), None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_spmv_rank_without_peers():
+    """A partition where ranks have no halo peers: the plan-time collective
+    keeps every rank in the communicator, the product is still bitwise."""
+    world = 3
+    a = W.block_diagonal([W.laplace7(5) for _ in range(world)])
+    x = np.random.default_rng(1).uniform(-1, 1, a.n)
+    want = oracle.spmv(a.row_start, a.col, a.val, x)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blockdiag_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    y = np.full(a.n, np.nan)
+    for rank, lo, hi, part, stats in got:
+        assert lo != "error", hi
+        assert stats["peers"] == 0
+        y[lo:hi] = part
+    assert np.array_equal(y, want)
+
+
+def _factor_records(shard, a):
+    """Oracle stand-in for the device plan: level-ordered front end, serial
+    factor and solves of the shard's block-diagonal matrix; per-system
+    records cut out by BatchShard."""
+    import hashlib
+    fe = oracle.front_end(a.n, a.row_start, a.col, a.val)
+    fval, bad = oracle.factor_serial(fe["row_start"], fe["col"], fe["val"], fe["diag"])
+    assert bad == -1
+    b = np.concatenate([np.random.default_rng(0).uniform(-1, 1, m) for m in shard.sizes])
+    b = b[fe["perm"]]
+    y = oracle.solve_forward(fe["row_start"], fe["col"], fval, b)
+    x, _ = oracle.solve_backward(fe["row_start"], fe["col"], fval, fe["diag"], y)
+    rows = shard.system_rows(fe["perm"])
+    h = lambda v: hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest()
+    return {sd: (h(shard.take_rows(fe["row_start"], fval, r)), h(x[r])) for sd, r in rows.items()}
+
+
+def _batch_worker(rank, world, port, count, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shard = jd.BatchShard(count, rank, world)
+        a = shard.assemble(lambda sd: W.rmat(9, sd))
+        recs = shard.gather(_factor_records(shard, a))
+        q.put((rank, shard.seeds, recs))
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_sharding_matches_single_process(world):
+    """c5-style batch sharding over gloo ranks: every rank factors and solves
+    its contiguous block of systems as one block-diagonal matrix; the
+    gathered per-system factor / solution digests equal those of each system
+    factored alone (and of the whole batch on one process)."""
+    count = 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, count, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    owned = []
+    for rank, seeds, recs in got:
+        assert seeds != "error", recs
+        owned += seeds
+        assert sorted(recs) == list(range(count))
+    assert sorted(owned) == list(range(count))
+    one = jd.BatchShard(count)
+    whole = _factor_records(one, one.assemble(lambda sd: W.rmat(9, sd)))
+    for sd in range(count):
+        alone = jd.BatchShard(1, first=sd)
+        rec = _factor_records(alone, alone.assemble(lambda s: W.rmat(9, s)))[sd]
+        assert whole[sd] == rec
+        for _, _, recs in got:
+            assert recs[sd] == rec

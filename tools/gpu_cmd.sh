@@ -1,4 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 600 python -m pytest tests/test_gpu_transfer.py tests/test_gpu_parity.py -q -x 2>&1 | tail -15
-for c in c2; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > gpurun_out/b_$c.json 2> gpurun_out/b_$c.err; echo "$c rc=$?"; tail -3 gpurun_out/b_$c.err; done
-python -c "import json; d=json.load(open('gpurun_out/b_c2.json')); print(d['e2e'], d['value'])"
+S=$SECONDS; timeout 900 python bench.py > gpurun_out/b_c2.json 2> gpurun_out/b_c2.err; echo "c2 rc=$? wall=$((SECONDS-S))"; tail -3 gpurun_out/b_c2.err
+S=$SECONDS; timeout 1200 python bench.py --config c5 --steps 5 > gpurun_out/b_c5.json 2> gpurun_out/b_c5.err; echo "c5 rc=$? wall=$((SECONDS-S))"; tail -3 gpurun_out/b_c5.err
