@@ -222,11 +222,12 @@ class DistSpmv:
             srs, scol, sval = _sub_csr(plan.rs, plan.col, plan.val, rows)
             self.parts.append((o.csr(srs, scol, sval), o.tensor_i32(rows)))
         self.send = [(q, o.tensor_i32(idx), idx.size, o.empty_f64(idx.size)) for q, idx in plan.send]
-        if plan.world > 1:
+        import torch.distributed as dist
+        if plan.world > 1 and dist.is_available() and dist.is_initialized():
             # NCCL requires the first collective on a communicator to include
             # every rank; a rank without halo peers would otherwise never
             # join it.  One tiny all-reduce at plan time initialises it.
-            import torch.distributed as dist
+            # (Without a process group: single-process emulation, tests.)
             probe = self.x_ext.new_zeros(1)
             dist.all_reduce(probe, group=group)
 
