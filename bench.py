@@ -544,7 +544,9 @@ def run_mine(args):
 
     def impl_of(sw):
         rp = ilu._region_for(sw)
-        return "tickets" if rp is None else ("two_stage" if rp is dv.TWO_STAGE else "region")
+        if rp is None:
+            return "tickets"
+        return "two_stage" if rp is dv.TWO_STAGE else ("cta" if rp is dv.CTA else "region")
     impl = {sw: impl_of(sw) for sw in ("factor", "fwd", "bwd")}
 
     # DAG depths and the measured cross-SM hop: depth x t_hop is the floor of
@@ -565,7 +567,8 @@ def run_mine(args):
     rooflines = {
         "factor": roof(ab["factor"], f_avg, fdepth,
                        {"tickets": "factor_kernel", "region": "region_kernel<0>",
-                        "two_stage": "factor_kernel + tail_upper_kernel"}[impl["factor"]],
+                        "two_stage": "factor_kernel + tail_upper_kernel + corner",
+                        "cta": "factor_cta_kernel"}[impl["factor"]],
                        "factor_dram_bytes"),
         "stri": roof(ab["stri"], st_avg, fdepth + bdepth,
                      f"fwd {impl['fwd']} + bwd {impl['bwd']}", "stri_dram_bytes"),

@@ -381,6 +381,39 @@ int jv_tail_upper(int64_t handle, const int32_t* col, const int32_t* diag_pos, d
 int jv_tail_corner(int64_t handle, int32_t* row_start, int32_t* col, int32_t* diag_pos,
                    int32_t* pos, void* stream);
 int jv_tail_plan_free(int64_t handle);
+/* ---- single-CTA level-synchronous kernels (small systems, the corner) --
+ * One thread block walks the levels of a sweep's DAG with __syncthreads
+ * between them (no cross-SM hops): factor_serial semantics
+ * (_kernels.py:165-204; thread per row, pivots ascending, updates in
+ * (pivot, q) order, tau / MILU as _factor_row) and the serial sweeps
+ * (_kernels.py:348-366).  Per level a precomputed program block
+ * (jv_cta_program_host, from the device update lists of jv_cta_plan_build
+ * exported by jv_cta_plan_export) is prefetched two levels ahead and the
+ * level's row data one level ahead with cp.async.  kind: 0 factor,
+ * 1 forward, 2 backward.  rb: depth of the row-data ring (2..6; the
+ * program ring is 2 rb - 1 deep); maxrows: rows of the widest level (sets the
+ * block width).  resident: values (factor) / the vector (solves)
+ * in shared memory for the whole sweep; jv_cta_smem gives the bytes a
+ * launch needs or -1 when it does not fit.  err_row: smallest zero-pivot
+ * row (atomicMin).  in may equal out. */
+int jv_cta_max_rows(void);
+int64_t jv_cta_plan_build(int32_t n, const int32_t* row_start, const int32_t* col,
+                          const int32_t* diag_pos, int milu, void* stream);
+int jv_cta_plan_export(int64_t handle, int32_t* lstart_h, int64_t* off_h, int32_t* otgt_h,
+                       int32_t* oq_h, int8_t* ok_h, int64_t* info_h);
+int jv_cta_plan_free(int64_t handle);
+int jv_cta_program_host(int kind, int32_t n, const int32_t* row_start_h, const int32_t* col_h,
+                        const int32_t* diag_h, const int32_t* order_h, const int32_t* level_ptr_h,
+                        int32_t nlev, const int32_t* lstart_h, const int64_t* off_h,
+                        const int32_t* otgt_h, const int32_t* oq_h, const int8_t* ok_h, int milu,
+                        int32_t* prog_h, int32_t* lbase_h, int64_t* sizes_h);
+int64_t jv_cta_smem(int kind, int32_t n, int64_t nnz, int32_t nlev, int64_t maxblk,
+                    int64_t maxstage, int resident, int rb);
+int jv_cta_run(int kind, int32_t n, int64_t nnz, int32_t nlev, const int32_t* prog,
+               const int32_t* lbase, int64_t maxblk, int64_t maxstage, int resident, int rb,
+               int32_t maxrows, double* val,
+               const double* norms, double tau, int milu, const double* in, double* out,
+               int32_t* err_row, void* stream);
 /* latency of one dependent cross-SM mailbox hop (ns), measured by a chain of
  * `hops` steps on consecutive SMs (synchronous; diagnostics for the bench's
  * depth x t_hop bound) */

@@ -249,6 +249,16 @@ def check_hang():
 # autotune candidate of the factorization: upper rows by the sync-free
 # kernel, then the two-stage lower tail (csrc/tail.cu)
 TWO_STAGE = {"two_stage": True, "nreg": 0}
+# autotune candidate of every sweep of a small matrix: one CTA walks the
+# levels with __syncthreads (csrc/cta.cu)
+CTA = {"cta": True, "nreg": 0}
+_CTA_MAX = []
+
+
+def cta_max_rows():
+    if not _CTA_MAX:
+        _CTA_MAX.append(int(_lib.load().jv_cta_max_rows()))
+    return _CTA_MAX[0]
 
 
 class TailPlan:
@@ -640,6 +650,8 @@ class DevIlu:
                 cands.append(rp)
         if sweep == "factor" and self.n_upper is not None and 0 < self.n_upper < self.n:
             cands.append(TWO_STAGE)
+        if 0 < self.n <= cta_max_rows() and self.cta_ok(sweep):
+            cands.append(CTA)
         if len(cands) == 1:
             self.autotune_ms[sweep] = ()
             return None
@@ -657,10 +669,14 @@ class DevIlu:
                     self._factor_tickets(0, self.n, 0, True)
                 elif rp is TWO_STAGE:
                     self.factor_two_stage_async(self.n_upper)
+                elif rp is CTA:
+                    self._factor_cta(True)
                 else:
                     self._factor_region(rp, True)
             elif rp is None:
                 self._solve_tickets(which, vin, vout)
+            elif rp is CTA:
+                self._solve_cta(which, vin, vout)
             else:
                 self._region_run(rp, 1 + which, vin, vout, self.sbox)
 
@@ -689,7 +705,7 @@ class DevIlu:
         best = cands[k] if times[k] < 0.97 * times[0] else None
         self.autotune_ms[sweep] = tuple(times)
         for k in [k for k, v in self._rstreams.items() if k[0] == sweep and v is not best
-                  and v is not TWO_STAGE]:
+                  and v is not TWO_STAGE and v is not CTA]:
             del self._rstreams[k]   # free the losing plans
         return best
 
@@ -852,6 +868,10 @@ class DevIlu:
             if rp is TWO_STAGE:
                 self.factor_two_stage_async(self.n_upper)
                 return
+            if rp is CTA:
+                self._factor_cta(norms)
+                self.values_changed()
+                return
             if rp is not None:
                 self._factor_region(rp, norms)
                 self.values_changed()
@@ -915,14 +935,20 @@ class DevIlu:
         if ev is not None:
             ev[1].record()
         c = tp.corner
+        c.tau, c.milu = self.tau, self.milu
+        # the corner's path (sync-free tickets or one CTA walking its
+        # levels) is timed once on its first use, before any value moves
+        mode = c._region_for("factor") if c.region_mode == "auto" else None
         if tp.nc:
             _lib.call("jv_gather", tp.nc, ptr(tp.pos), ptr(self.val), ptr(c.val), stream())
             tp.save.copy_(c.val[:tp.nc])
         c.values_changed()
         if self.tau > 0:
             c.norms[:tp.nt].copy_(self.norms[n_upper:self.n])
-        c.tau, c.milu = self.tau, self.milu
-        c._factor_tickets(0, tp.nt, 0, False)
+        if mode is CTA:
+            c._factor_cta(False)
+        else:
+            c._factor_tickets(0, tp.nt, 0, False)
         if tp.nc:
             _lib.call("jv_scatter", tp.nc, ptr(tp.pos), ptr(c.val), ptr(self.val), stream())
         if ev is not None:
@@ -955,6 +981,107 @@ class DevIlu:
             self._factor_tickets(0, n_upper, 0, True)
         self.factor_tail_async(n_upper, norms=(n_upper == 0), ev=ev)
         self.values_changed()
+
+    # single-CTA level-synchronous kernels (csrc/cta.cu) -----------------
+    CTA_RINGS = (5, 4, 3, 2)    # row-data ring depths tried, deepest first
+
+    def cta_programs(self):
+        """Level programs of the single-CTA kernels per sweep ("factor",
+        "fwd", "bwd") -> dict(prog, lbase, nlev, maxblk, maxstage, resident)
+        or None when that sweep does not fit one CTA (cached per MILU)."""
+        key = bool(self.milu)
+        if getattr(self, "_cta", None) is not None and self._cta[0] == key:
+            return self._cta[1]
+        lib = _lib.load()
+        t = torch()
+        out = {"factor": None, "fwd": None, "bwd": None}
+        if 0 < self.n <= cta_max_rows():
+            h = lib.jv_cta_plan_build(self.n, ptr(self.row_start), ptr(self.col),
+                                      ptr(self.diag_pos), int(self.milu), stream())
+            if h <= 0:
+                raise RuntimeError(f"jv_cta_plan_build failed ({h}): "
+                                   f"{lib.jv_last_error().decode(errors='replace')}")
+            try:
+                out = self._cta_build(lib, h)
+            finally:
+                lib.jv_cta_plan_free(h)
+        self._cta = (key, out)
+        return out
+
+    def _cta_build(self, lib, h):
+        """Host-side program build from the device update lists (setup)."""
+        t = torch()
+        rs, col, dg = (np.ascontiguousarray(x) for x in self._host_pattern())
+        n, nnz = self.n, self.nnz
+        lens = rs[1:].astype(np.int64) - rs[:-1]
+        nL = dg.astype(np.int64) - rs[:-1]
+        # the device plan's lists, copied back once (small matrices only)
+        ptrs = self._cta_lists(h, lib, int(nL.sum()))
+        if self._fwd_levels is None:
+            self._fwd_levels, _ = levels_dev(self.pattern, False)
+        out = {}
+        bl, nb = levels_dev(self.pattern, True)
+        for sweep, lev in (("factor", self._fwd_levels), ("fwd", self._fwd_levels), ("bwd", bl)):
+            nlev = int(lev.max().item()) + 1
+            o, lp = level_sort_dev(n, nlev, lev)
+            order = np.ascontiguousarray(o[:n].cpu().numpy(), dtype=np.int32)
+            lptr = np.ascontiguousarray(lp[:nlev + 1].cpu().numpy(), dtype=np.int32)
+            kind = {"factor": 0, "fwd": 1, "bwd": 2}[sweep]
+            sizes = (ctypes.c_int64 * 3)()
+            args = [kind, n, _hp(rs), _hp(col), _hp(dg), _hp(order), _hp(lptr), nlev,
+                    *ptrs, int(self.milu)]
+            _lib.call("jv_cta_program_host", *args, None, None, sizes)
+            total, maxblk, maxstage = (int(v) for v in sizes)
+            prog = np.empty(max(total, 4), dtype=np.int32)
+            lbase = np.empty(nlev + 1, dtype=np.int32)
+            _lib.call("jv_cta_program_host", *args, _hp(prog), _hp(lbase), sizes)
+            # deepest pipeline that fits, values resident in shared memory first
+            fit = [(res, rb) for res in (1, 0) for rb in self.CTA_RINGS
+                   if lib.jv_cta_smem(kind, n, nnz, nlev, maxblk, maxstage, res, rb) >= 0]
+            if not fit:
+                out[sweep] = None
+                continue
+            resident, rb = fit[0]
+            up = lambda a: t.from_numpy(a).to("cuda")
+            out[sweep] = dict(kind=kind, prog=up(prog), lbase=up(lbase), nlev=nlev, maxblk=maxblk,
+                              maxstage=maxstage, resident=resident, rb=rb,
+                              maxrows=int(np.diff(lptr).max()) if nlev else 0)
+        return out
+
+    def _cta_lists(self, h, lib, nl):
+        """Host copies (lstart, off, otgt, oq, ok) of the update lists."""
+        info = (ctypes.c_int64 * 4)()
+        _lib.call("jv_cta_plan_export", h, None, None, None, None, None, info)
+        nops = int(info[1])
+        lstart = np.empty(self.n + 1, np.int32)
+        off = np.empty(nl + 1, np.int64)
+        otgt = np.empty(max(nops, 1), np.int32)
+        oq = np.empty(max(nops, 1), np.int32)
+        ok = np.zeros(max(nops, 1), np.int8)
+        _lib.call("jv_cta_plan_export", h, _hp(lstart), _hp(off), _hp(otgt), _hp(oq), _hp(ok), info)
+        self._cta_keep = (lstart, off, otgt, oq, ok)
+        return [_hp(lstart), _hp(off), _hp(otgt), _hp(oq), _hp(ok)]
+
+    def cta_ok(self, sweep):
+        return self.cta_programs().get(sweep) is not None
+
+    def _cta_run(self, sweep, inp=None, out=None):
+        g = self.cta_programs()[sweep]
+        _lib.call("jv_cta_run", g["kind"], self.n, self.nnz, g["nlev"], ptr(g["prog"]),
+                  ptr(g["lbase"]), g["maxblk"], g["maxstage"], g["resident"], g["rb"], g["maxrows"],
+                  ptr(self.val),
+                  ptr(self.norms), self.tau, int(self.milu), ptr(inp), ptr(out), ptr(self.err),
+                  stream())
+
+    def _factor_cta(self, norms, reset=True):
+        if norms and self.tau > 0:
+            self.compute_norms()
+        if reset:
+            _lib.call("jv_reset_row", ptr(self.err), stream())
+        self._cta_run("factor")
+
+    def _solve_cta(self, which, b, out):
+        self._cta_run("fwd" if which == 0 else "bwd", b, out)
 
     # streamed drop-in factorization: host values in, factors out -------
     STREAM_CHUNKS = 8
@@ -1060,6 +1187,9 @@ class DevIlu:
 
     def solve_async(self, which, b, out):
         rp = self._region_for("fwd" if which == 0 else "bwd")
+        if rp is CTA:
+            self._solve_cta(which, b, out)
+            return out
         if rp is not None:
             # the backward sweep's value pack depends only on the factors:
             # refresh it on a side stream while the forward region kernel
