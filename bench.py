@@ -271,8 +271,7 @@ def parity_check(cfg, ilu, plan, x, sy, blocks, n):
         r = rows[sd]
         ok &= digest(blocks.take_rows(rs, val, r), "f") == d["fval"]
         ok &= digest(xh[r], "f") == d["x"]
-        # the block's spmv rows: hub rows beyond one tile are tree-summed
-        # (1e-12), so the spmv digest is informative only
+        ok &= digest(syh[r], "f") == d["spmv_perm"]
     return bool(ok)
 
 

@@ -9,9 +9,9 @@
 // shared memory, then each row is summed serially from shared memory by one
 // thread in the reference order — so every row of up to kTile+1 entries is
 // BITWISE equal to the reference while global traffic stays at the
-// 12 nnz + 20 n algorithmic bytes.  A row longer than kTile (R-MAT hubs) is
-// reduced by the whole CTA as a tree (within the 1e-12 the north star allows
-// for fp64 sums).  The tile -> first-row map is a setup-time plan
+// 12 nnz + 20 n algorithmic bytes.  A row longer than kTile (R-MAT hubs)
+// has its products formed by the whole CTA chunk by chunk and summed by one
+// thread in order, so it is bitwise too.  The tile -> first-row map is a setup-time plan
 // (jv_spmv_plan); without it each CTA binary-searches row_start.
 #include "common.cuh"
 #include "../../include/jv.h"
@@ -54,7 +54,6 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
     const int32_t* __restrict__ tile_rows, const int32_t* __restrict__ row_map) {
   __shared__ double prod[kBuf];
-  __shared__ double red[kSpmvThreads / 32];
   const int t = blockIdx.x;
   const int ntiles = gridDim.x;
   int r0, r1, p0, p1;
@@ -111,19 +110,21 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
     __stcs(y + (row_map ? __ldg(row_map + r) : r), s);
   }
   if (rlast == r1) return;
-  // long row: strided partial sums, warp tree, then the 8 warp sums in order
+  // a row longer than a tile (R-MAT hubs): its products chunk by chunk in
+  // shared memory (all threads, coalesced), summed serially by one thread in
+  // the reference order — bitwise like every other row
   const int a = __ldg(rs + rlast), b = __ldg(rs + rlast + 1);
-  double s = 0.0;
-  for (int q = a + threadIdx.x; q < b; q += kSpmvThreads)
-    s = jv::dadd(s, jv::dmul(__ldcs(val + q), __ldg(x + __ldcs(col + q))));
-  for (int o = 16; o > 0; o >>= 1) s = jv::dadd(s, __shfl_xor_sync(0xffffffffu, s, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int w = 0; w < kSpmvThreads / 32; ++w) tot = jv::dadd(tot, red[w]);
-    y[row_map ? row_map[rlast] : rlast] = tot;
+  double acc = 0.0;
+  for (int c0 = a; c0 < b; c0 += kBuf) {
+    const int c1 = c0 + kBuf < b ? c0 + kBuf : b;
+    __syncthreads();
+    for (int q = c0 + threadIdx.x; q < c1; q += kSpmvThreads)
+      prod[q - c0] = jv::dmul(__ldcs(val + q), __ldg(x + __ldcs(col + q)));
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < c1 - c0; ++q) acc = jv::dadd(acc, prod[q]);
   }
+  if (threadIdx.x == 0) y[row_map ? row_map[rlast] : rlast] = acc;
 }
 
 }  // namespace

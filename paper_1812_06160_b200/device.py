@@ -984,6 +984,7 @@ class DevIlu:
 
     # single-CTA level-synchronous kernels (csrc/cta.cu) -----------------
     CTA_RINGS = (5, 4, 3, 2)    # row-data ring depths tried, deepest first
+    CTA_MAX_PROGRAM = 1 << 26   # ints of level programs worth building
 
     def cta_programs(self):
         """Level programs of the single-CTA kernels per sweep ("factor",
@@ -1016,12 +1017,16 @@ class DevIlu:
         lens = rs[1:].astype(np.int64) - rs[:-1]
         nL = dg.astype(np.int64) - rs[:-1]
         # the device plan's lists, copied back once (small matrices only)
-        ptrs = self._cta_lists(h, lib, int(nL.sum()))
         if self._fwd_levels is None:
             self._fwd_levels, _ = levels_dev(self.pattern, False)
         out = {}
         bl, nb = levels_dev(self.pattern, True)
+        self._cta_nofactor = False
+        ptrs = self._cta_lists(h, lib, int(nL.sum()))
         for sweep, lev in (("factor", self._fwd_levels), ("fwd", self._fwd_levels), ("bwd", bl)):
+            if sweep == "factor" and self._cta_nofactor:
+                out[sweep] = None
+                continue
             nlev = int(lev.max().item()) + 1
             o, lp = level_sort_dev(n, nlev, lev)
             order = np.ascontiguousarray(o[:n].cpu().numpy(), dtype=np.int32)
@@ -1030,8 +1035,13 @@ class DevIlu:
             sizes = (ctypes.c_int64 * 3)()
             args = [kind, n, _hp(rs), _hp(col), _hp(dg), _hp(order), _hp(lptr), nlev,
                     *ptrs, int(self.milu)]
-            _lib.call("jv_cta_program_host", *args, None, None, sizes)
+            if lib.jv_cta_program_host(*args, None, None, sizes) != 0:
+                out[sweep] = None          # too large for the single-CTA path
+                continue
             total, maxblk, maxstage = (int(v) for v in sizes)
+            if total > self.CTA_MAX_PROGRAM or 3 * 4 * maxblk > 200 * 1024:
+                out[sweep] = None          # a level block cannot fit shared memory
+                continue
             prog = np.empty(max(total, 4), dtype=np.int32)
             lbase = np.empty(nlev + 1, dtype=np.int32)
             _lib.call("jv_cta_program_host", *args, _hp(prog), _hp(lbase), sizes)
@@ -1053,12 +1063,18 @@ class DevIlu:
         info = (ctypes.c_int64 * 4)()
         _lib.call("jv_cta_plan_export", h, None, None, None, None, None, info)
         nops = int(info[1])
+        if 2 * nops > self.CTA_MAX_PROGRAM:
+            nops, nl = 0, 0     # the factor program would not fit: lists not needed
         lstart = np.empty(self.n + 1, np.int32)
         off = np.empty(nl + 1, np.int64)
         otgt = np.empty(max(nops, 1), np.int32)
         oq = np.empty(max(nops, 1), np.int32)
         ok = np.zeros(max(nops, 1), np.int8)
-        _lib.call("jv_cta_plan_export", h, _hp(lstart), _hp(off), _hp(otgt), _hp(oq), _hp(ok), info)
+        if nl or nops:
+            _lib.call("jv_cta_plan_export", h, _hp(lstart), _hp(off), _hp(otgt), _hp(oq), _hp(ok),
+                      info)
+        else:
+            self._cta_nofactor = True
         self._cta_keep = (lstart, off, otgt, oq, ok)
         return [_hp(lstart), _hp(off), _hp(otgt), _hp(oq), _hp(ok)]
 
