@@ -82,25 +82,31 @@ JV_INLINE void bar_wait(uint64_t* b, uint32_t parity) {
       "RW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra RW_%=;\n}" ::"r"(sa(b)), "r"(parity) : "memory");
 }
-// wave block view (regions_host.cpp): SoA arrays of cnt rows
+// wave block view (regions_host.cpp): header, 32-byte row records
+// {ref0..ref3, p0, row, meta, me}, xref[K - 4][cnt], pslot[NP]; refs and
+// `me` are byte offsets into the CTA's shared memory
 struct Wave {
   const int32_t* b;
   int cnt, slot0, K, NP;
   JV_INLINE Wave(const unsigned char* p) : b(reinterpret_cast<const int32_t*>(p)) {
-    cnt = b[0];
-    slot0 = b[1];
-    K = b[2];
-    NP = b[3];
+    const int4 h = *reinterpret_cast<const int4*>(p);
+    cnt = h.x;
+    slot0 = h.y;
+    K = h.z;
+    NP = h.w;
   }
-  JV_INLINE int row(int i) const { return b[4 + i]; }
-  JV_INLINE int p0(int i) const { return b[4 + cnt + i]; }
-  JV_INLINE int meta(int i) const { return b[4 + 2 * cnt + i]; }
-  JV_INLINE int ref(int k, int i) const { return b[4 + (3 + k) * cnt + i]; }
-  template <int KIND>
-  JV_INLINE int pslot(int j) const { return b[4 + (3 + K) * cnt + j]; }
+  JV_INLINE const int4* rec(int i) const { return reinterpret_cast<const int4*>(b + 4) + 2 * i; }
+  JV_INLINE const int32_t* xref() const { return b + 4 + 8 * cnt; }
+  JV_INLINE int pslot(int j) const { return b[4 + (8 + max(K - 4, 0)) * cnt + j]; }
 };
+#ifndef JV_RDIAG
+#define JV_RDIAG 0   // diagnostic builds strip parts of the compute loop (wrong results)
+#endif
+constexpr int kOneOff = 144;   // shared-memory offset of the constant 1.0
 constexpr int kCompute = 512;
-constexpr int kBlock = kCompute + 64;   // + a producer warp (one lane) and a prober warp
+constexpr int kProbers = 4;             // prober warps; warp p owns the waves w with w % kProbers == p
+constexpr int kExtra = 32 + 32 * kProbers;   // a producer warp (one lane) and the prober warps
+constexpr int kBlock = kCompute + kExtra;
 constexpr int kWin = 4;                 // prober window (waves; 16 and 2 measured slower on c2)
 
 JV_INLINE void cp16(void* dst, const void* src) {
@@ -136,17 +142,16 @@ JV_INLINE int ld_volatile_shared(const int* p) {
 // compute warps (whose progress it reads from a shared counter before
 // reusing ring space), with L2 bulk prefetches kL2 waves further ahead.
 template <int KIND, int NC = kCompute>
-__global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
+__global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
   constexpr int kCompute = NC;   // compute threads: waves of at most NC rows
   extern __shared__ __align__(128) unsigned char rsm[];
   const unsigned full = 0xffffffffu;
   const int tid = threadIdx.x;
   uint64_t* bar = reinterpret_cast<uint64_t*>(rsm);            // wave full [kNB]
   int* done = reinterpret_cast<int*>(rsm + 8 * kNB);          // waves finished
-  int* probed = done + 1;   // waves below are released by the prober
   int* issued = done + 2;   // waves whose blocks the producer has issued
+  int* probed = done + 8;   // [kProbers] per prober warp: its waves below this are released
   int4* tab = reinterpret_cast<int4*>(rsm + 256);             // 2 per wave
-  double* slot = reinterpret_cast<double*>(rsm + 256 + 32 * A.max_waves);
   unsigned char* sring = rsm + 256 + 32 * A.max_waves + 8 * A.SC;
   unsigned char* dring = sring + A.CS;
   const int w0 = A.reg_wave[blockIdx.x];
@@ -155,8 +160,9 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
   if (tid == 0) {
     for (int b = 0; b < kNB; ++b) bar_init(&bar[b], 1);
     *done = 0;
-    *probed = 0;
+    for (int p = 0; p < kProbers; ++p) probed[p] = 0;
     *issued = 0;
+    *reinterpret_cast<double*>(rsm + kOneOff) = 1.0;   // the unused refs of short rows
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -174,7 +180,16 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
     // packets are current.  Decoupled from the compute warps' barrier
     // cadence, so a value published upstream reaches a waiting wave within
     // about one round trip, and values published earlier cost nothing.
-    const int lane = tid - kCompute - 32;
+    // Several prober warps share the work: warp p owns the waves w with
+    // w % kProbers == p (its own window, its own release counter), so their
+    // round trips overlap and the window reaches kWin * kProbers waves
+    // ahead — a single warp's round (fetch, L2 round trip, check, decode)
+    // takes about as long as three waves of compute and was the pacemaker
+    // of every region but the first (measured: a stall every third wave).
+    const int lane = tid & 31;
+    const int pw = (tid - kCompute - 32) >> 5;
+    constexpr int P = kProbers;
+    int* const myprobed = probed + pw;
     auto pkts = [&](int x) -> unsigned char* {
       const int4 v = tab[2 * x + 1];
       return dring + tab[2 * x].w + v.y + (v.w & 0xffff);
@@ -184,8 +199,13 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
       const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(p);
       return (uint32_t)(q.x >> 32) == A.epoch && (uint32_t)(q.y >> 32) == A.epoch;
     };
-    int lo = 0, hi = 0;
+    int lo = pw, hi = pw;
     unsigned ns = 0, spins = 0;
+    if (flags & 8) {   // diagnostic: no remote waits at all (wrong results)
+      if (lane == 0)
+        asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(nw + P) : "memory");
+      return;
+    }
     while (lo < nw) {
       // admit waves: one without remote dependencies needs nothing; one with
       // them once the producer has issued it and its blocks are in (its
@@ -193,27 +213,27 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
       bool issued_any = false;
       const int hi0 = hi;
       const int iss = ld_volatile_shared(issued);
-      while (hi < nw && hi < lo + kWin) {
+      while (hi < nw && hi < lo + kWin * P) {
         if (np(hi) > 0) {
           if (hi >= iss || !bar_test(&bar[hi % kNB], (uint32_t)((hi / kNB) & 1))) break;
           const Wave X(sring + tab[2 * hi].z);
           unsigned char* pk = pkts(hi);
           if (!(flags & 8))
             for (int j = lane; j < X.NP; j += 32) {
-              cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot<KIND>(j));
+              cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot(j));
               issued_any = true;
             }
         }
-        ++hi;
+        hi += P;
       }
       // one round: copy every stale packet of the window
-      for (int x = lo; x < hi0; ++x) {
+      for (int x = lo; x < hi0; x += P) {
         if (np(x) == 0) continue;
         const Wave X(sring + tab[2 * x].z);
         unsigned char* pk = pkts(x);
         for (int j = lane; j < X.NP; j += 32)
           if (!fresh(pk + 16 * j) && !(flags & 8)) {
-            cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot<KIND>(j));
+            cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot(j));
             issued_any = true;
           }
       }
@@ -229,13 +249,20 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
           bool ok = true;
           for (int j = lane; j < X.NP; j += 32) ok = ok && ((flags & 8) || fresh(pk + 16 * j));
           if (!__all_sync(full, ok)) break;
+          // decoded values behind the packets: what the rows' refs point to
+          double* rem = reinterpret_cast<double*>(const_cast<unsigned char*>(pk) + 16 * X.NP);
+          for (int j = lane; j < X.NP; j += 32) {
+            const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(pk + 16 * j);
+            rem[j] = __longlong_as_double((long long)((q.x & 0xffffffffull) | (q.y << 32)));
+          }
         }
-        ++lo;
+        lo += P;
       }
       if (lo != lo0) {
+        __syncwarp();
         if (lane == 0) {
           // release: the packets written above are visible to whoever acquires
-          asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(sa(probed)), "r"(lo) : "memory");
+          asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(lo) : "memory");
         }
         ns = 0;
         spins = 0;
@@ -246,7 +273,7 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
         if (++spins == jv::g_spin_limit) {
           atomicExch(&jv::g_hang, 1);
           if (lane == 0)
-            asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(probed)), "r"(nw) : "memory");
+            asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(nw + P) : "memory");
           break;
         }
       }
@@ -262,9 +289,11 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
       if (v2.y > 0) l2_prefetch_bulk(A.pack + 2 * (int64_t)v2.x, (uint32_t)v2.y);
       if (v2.w & 0xffff) l2_prefetch_bulk(A.vpack + 2 * (int64_t)v2.z, (uint32_t)(v2.w & 0xffff));
     };
-    for (int x = 0; x < kL2 && x < nw; ++x) prefetch(x);
+    // (diagnostics: flags bits 8..15 override the L2 prefetch distance, 255 = none)
+    const int kl2 = ((flags >> 8) & 255) == 255 ? 0 : ((flags >> 8) & 255) ? (int)((flags >> 8) & 255) : kL2;
+    for (int x = 0; x < kl2 && x < nw; ++x) prefetch(x);
     for (int x = 0; x < nw; ++x) {
-      if (x + kL2 < nw) prefetch(x + kL2);
+      if (kl2 && x + kl2 < nw) prefetch(x + kl2);
       // ring blocks of wave x may overlap those of wave x - D - 1
       while (ld_volatile_shared(done) < x - D) __nanosleep(20);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -283,113 +312,186 @@ __global__ void __launch_bounds__(NC + 64, 1) region_kernel(RArgs A) {
   }
 
   // -------------------------------------------------------------- compute
-  constexpr int kR = 4;   // register fast path: dependencies per row
-  const jv::Trace T = jv::trace_begin();
-  for (int w = 0; w < nw; ++w) {
-    if (tid == 0) jv::trace_mark(T, w0 + w, 1);
+  // One row per thread, one warp per scheduler: nothing hides a stall, so
+  // the wave loop is written as straight-line code — every shared-memory
+  // access is an explicit ld/st.shared at a precomputed offset (program
+  // order = issue order), a wave's operands (its 32-byte record, matrix
+  // values, right-hand side) are loaded into registers while the wave
+  // before it computes, the two operand sets ping-pong (no copies), threads
+  // beyond a wave's rows redo its last row with their stores predicated
+  // off, and the only branches are the remote-wave wait, the rare slow
+  // division and the rare zero pivot.  Critical path per wave:
+  //   barrier -> dependency loads -> arithmetic chain -> slot store -> barrier.
+  constexpr int kR = 4;   // dependencies held in registers
+  const uint32_t sb = sa(rsm);
+  auto lds64 = [&](uint32_t off) -> double {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(sb + off));
+    return v;
+  };
+  auto lds128 = [&](uint32_t off) -> int4 {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(sb + off));
+    return v;
+  };
+  const uint32_t tab_off = 256, sring_off = (uint32_t)(sring - rsm), dring_off = (uint32_t)(dring - rsm);
+  struct Ops {
+    int cnt, K, np;
+    int4 r0, r1;          // {ref0..3}, {p0, row, meta, me}
+    double a[kR], u[kR], dg, rhs;
+    const int32_t* xref;
+    const double* vals;
+  };
+  auto fetch = [&](int w, Ops& s) {
     bar_wait(&bar[w % kNB], (uint32_t)((w / kNB) & 1));
-    const int4 t = tab[2 * w];
-    const int4 tv = tab[2 * w + 1];
-    const Wave V(sring + t.z);
-    const int cnt = V.cnt, K = V.K;
-    const bool active = tid < cnt;
-    const double* vals = reinterpret_cast<const double*>(dring + t.w);
-    const double* vec = reinterpret_cast<const double*>(dring + t.w + tv.y);
-    const unsigned char* pk = dring + t.w + tv.y + (tv.w & 0xffff);
-    auto val = [&](int k) -> double { return vals[k * cnt + tid]; };
-    auto packet = [&](int j) -> double {
-      const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(pk + 16 * j);
-      return __longlong_as_double((long long)((p.x & 0xffffffffull) | (p.y << 32)));
-    };
-    if (tid == 0) jv::trace_mark(T, w0 + w, 2);
+    const int4 t = lds128(tab_off + 32 * w);
+    const int4 tv = lds128(tab_off + 32 * w + 16);
+    const uint32_t blk = sring_off + t.z;
+    const int4 hd = lds128(blk);   // cnt, slot0, K, NP
+    const int cnt = hd.x, K = hd.z;
+    s.cnt = cnt;
+    s.K = K;
+    s.np = hd.w;
+    s.xref = reinterpret_cast<const int32_t*>(rsm + blk) + 4 + 8 * cnt;
+    s.vals = reinterpret_cast<const double*>(rsm + dring_off + t.w);
+    // threads beyond the wave take its last row's operands
+    const int i = min(tid, cnt - 1);
+    s.r0 = lds128(blk + 16 + 32 * i);
+    s.r1 = lds128(blk + 32 + 32 * i);
+    const uint32_t vp = dring_off + t.w + 8 * i;   // vals[k][i] at vp + 8 * k * cnt
+    const uint32_t c8 = 8 * cnt;
+    const uint32_t vec = dring_off + t.w + tv.y + 8 * i;
+    if (KIND == 0) {
+      // a_k, a_rr, u_k in vals[2K + 1][cnt]; the pack holds +0.0 for the
+      // entries of rows with fewer than K pivots
+#pragma unroll
+      for (int k = 0; k < kR; ++k) {
+        s.a[k] = lds64(vp + min(k, max(K, 1) - 1) * c8);
+        s.u[k] = lds64(vp + (K + min(k + 1, K)) * c8);
+      }
+      s.dg = lds64(vp + K * c8);
+      s.rhs = lds64(tau ? vec : vp);   // the row's norm when tau > 0 (no vector block otherwise)
+    } else {
+      const int o = KIND == 1 ? 0 : 1;
+#pragma unroll
+      for (int k = 0; k < kR; ++k) s.a[k] = lds64(vp + (o + min(k, max(K, 1) - 1)) * c8);
+      s.dg = lds64(vp);
+      s.rhs = lds64(vec);
+    }
+  };
+  double* const gval = A.val;
+  double* const gout = A.out;
+  uint64_t* const mbox = A.mbox;
+  const uint32_t epoch = A.epoch;
+  const double tauv = tau ? A.tau : 0.0;
+#ifdef JV_REGION_TRACE
+  const jv::Trace T = jv::trace_begin();
+  const bool tracing = T.p != nullptr && tid == 0;
+#endif
+  auto step = [&](int w, const Ops& cur, Ops& nxt) {
     // the prober has released this wave's remote dependencies (a wave
-    // without any passes straight through; the prober never reads its ring
-    // blocks, so their reuse needs no handshake)
-    if ((tv.w >> 16) > 0) {
-      while (ld_acquire_shared(probed) <= w) {
+    // without any passes straight through)
+    if (cur.np > 0) {
+      const int* const pr = probed + (w % kProbers);
+      while (ld_acquire_shared(pr) <= w) {
       }
     }
     double dv[kR];
-    int nd = 0, meta = 0;
-    if (active) {
-      meta = V.meta(tid);
-      nd = meta & 63;
-      // branch-free: every ref load, then both candidate values of every
-      // dependency (slot ring and packet; both addresses are in shared
-      // memory), then selects -- two load latencies instead of a chain
-      int ref[kR];
+    dv[0] = lds64(cur.r0.x);
+    dv[1] = lds64(cur.r0.y);
+    dv[2] = lds64(cur.r0.z);
+    dv[3] = lds64(cur.r0.w);
+    // the next wave's operands, in flight during this wave's arithmetic
+    // (after the last wave: that wave again, its blocks are still there)
+#if (JV_RDIAG & 1)
+    nxt = cur;
+#else
+    fetch(min(w + 1, nw - 1), nxt);
+#endif
+    const int cnt = cur.cnt, K = cur.K;
+    const bool active = tid < cnt;
+    const int meta = cur.r1.z, nd = meta & 63, row = cur.r1.y, p0 = cur.r1.x;
+    const bool pub = active && (meta & 64);
+    double res;
+#if (JV_RDIAG & 2)
+    res = cur.dg + dv[0] + dv[1] + dv[2] + dv[3] + cur.a[0] + cur.u[0] + cur.rhs;
+    if (false) {
+#else
+    if (KIND == 0) {
+#endif
+      // pivots beyond the row's own: a = +0.0 (K > k >= nd) or a copy of an
+      // earlier operand (k >= K), never used: umask and the stores are per nd
+      double l[4];
+      {
+        double a3[3] = {cur.a[0], cur.a[1], cur.a[2]}, d3[3] = {dv[0], dv[1], dv[2]}, l3[3];
+        jv::ddiv_batch<3>(a3, d3, l3, nd);
+        l[0] = l3[0];
+        l[1] = l3[1];
+        l[2] = l3[2];
+        l[3] = 0.0;
+        if (K > 3) l[3] = jv::ddiv(cur.a[3], dv[3]);
+      }
+      const double thresh = jv::dmul(tauv, cur.rhs);
+      double d = cur.dg;
+      const int umask = (meta >> 7) & 15;
 #pragma unroll
-      for (int k = 0; k < kR; ++k) ref[k] = k < nd ? V.ref(k, tid) : 0;
-      double sv[kR];
-      ulonglong2 pv[kR];
+      for (int k = 0; k < 4; ++k) {
+        const bool drop = tau && fabs(l[k]) < thresh;
+        const double dn = jv::dsub(d, jv::dmul(l[k], cur.u[k]));
+        d = (!drop && (umask & (1 << k))) ? dn : d;
+        l[k] = drop ? 0.0 : l[k];
+      }
+      res = d;
+#if !(JV_RDIAG & 4)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (active && k < nd) __stcg(gval + p0 + k, l[k]);
+      if (active) __stcg(gval + p0 + nd, d);
+      if (active && d == 0.0) atomicMin(A.err, row);
+#endif
+    } else {
+      // unused refs read 1.0 against a packed +0.0 (or, beyond K, a copy of
+      // an operand, masked here): s - 0 = s exactly
+      const int o = KIND == 1 ? 0 : 1;
+      double sacc = cur.rhs;
 #pragma unroll
       for (int k = 0; k < kR; ++k) {
-        sv[k] = slot[max(ref[k], 0)];
-        // (a wave without packets may end at the ring's end: read the
-        // slot ring instead, the value is discarded)
-        pv[k] = *reinterpret_cast<const ulonglong2*>(
-            V.NP > 0 ? pk + 16 * max(-1 - ref[k], 0) : reinterpret_cast<const unsigned char*>(slot));
+        const double sn = jv::dsub(sacc, jv::dmul(cur.a[k], dv[k]));
+        sacc = k < nd ? sn : sacc;
       }
-#pragma unroll
-      for (int k = 0; k < kR; ++k) {
-        const double p = __longlong_as_double(
-            (long long)((pv[k].x & 0xffffffffull) | (pv[k].y << 32)));
-        dv[k] = k < nd ? (ref[k] >= 0 ? sv[k] : p) : 1.0;
+      if (K > kR && active) {
+        for (int k = kR; k < nd; ++k)
+          sacc = jv::dsub(sacc, jv::dmul(cur.vals[(o + k) * cnt + tid],
+                                         lds64((uint32_t)cur.xref[(k - kR) * cnt + tid])));
       }
+      if (KIND == 2) sacc = jv::ddiv(sacc, cur.dg);
+      res = sacc;
+      if (active) __stcg(gout + row, sacc);
     }
-    if (tid == 0) jv::trace_mark(T, w0 + w, 3);
-    if (active) {
-      const int me = (V.slot0 + tid) & (A.SC - 1);
-      const int p0 = V.p0(tid);
-      if (KIND == 0) {
-        double a[4], u[4], l[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          a[k] = k < nd ? val(k) : 0.0;
-          u[k] = k < nd ? val(K + 1 + k) : 0.0;
-        }
-        jv::ddiv_batch<4>(a, dv, l, nd);
-        const double thresh = tau ? jv::dmul(A.tau, vec[tid]) : 0.0;
-        double d = val(K);
-        const int umask = (meta >> 7) & 15;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (k < nd) {
-            if (tau && fabs(l[k]) < thresh) l[k] = 0.0;
-            else if (umask & (1 << k)) d = jv::dsub(d, jv::dmul(l[k], u[k]));
-          }
-        }
-        slot[me] = d;
-        if (meta & 64) jv::mbox_put(A.mbox, V.row(tid), d, A.epoch);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k < nd) __stcg(A.val + p0 + k, l[k]);
-        __stcg(A.val + p0 + nd, d);
-        if (d == 0.0) atomicMin(A.err, V.row(tid));
-      } else {
-        const int o = KIND == 1 ? 0 : 1;
-        double sacc = vec[tid];
-#pragma unroll
-        for (int k = 0; k < kR; ++k)
-          if (k < nd) sacc = jv::dsub(sacc, jv::dmul(val(o + k), dv[k]));
-        for (int k = kR; k < nd; ++k) {
-          const int ref = V.ref(k, tid);
-          const double x = ref >= 0 ? slot[ref] : packet(-1 - ref);
-          sacc = jv::dsub(sacc, jv::dmul(val(o + k), x));
-        }
-        if (KIND == 2) sacc = jv::ddiv(sacc, val(0));
-        slot[me] = sacc;
-        const int r = V.row(tid);
-        if (meta & 64) jv::mbox_put(A.mbox, r, sacc, A.epoch);
-        __stcg(A.out + r, sacc);
-      }
-    }
-    if (tid == 0) jv::trace_mark(T, w0 + w, 4);
+    if (active) asm volatile("st.shared.f64 [%0], %1;" ::"r"(sb + (uint32_t)cur.r1.w), "d"(res) : "memory");
+#if !(JV_RDIAG & 4)
+    if (pub) jv::mbox_put(mbox, row, res, epoch);
+#endif
+#if !(JV_RDIAG & 8)
     asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
+#endif
     if (tid == 0) {
       asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(done)), "r"(w + 1) : "memory");
-      jv::trace_mark(T, w0 + w, 7);
+#ifdef JV_REGION_TRACE
+      if (tracing) jv::trace_clock(T, w0 + w, 7);
+#endif
     }
+  };
+  if (nw > 0) {
+    Ops oa, ob;
+    fetch(0, oa);
+    int w = 0;
+    for (; w + 1 < nw; w += 2) {
+      step(w, oa, ob);
+      step(w + 1, ob, oa);
+    }
+    if (w < nw) step(w, oa, ob);
   }
 }
 
@@ -499,7 +601,7 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const
   // barrier, no idle warps
   const int nc = max_rows > 0 && max_rows <= 128 ? 128
                  : max_rows > 0 && max_rows <= 256 ? 256 : jvr::kCompute;
-  const int block = nc + 64;
+  const int block = nc + jvr::kExtra;
   const void* fn =
       nc == 128 ? (kind == 0 ? (const void*)jvr::region_kernel<0, 128>
                              : kind == 1 ? (const void*)jvr::region_kernel<1, 128>

@@ -18,17 +18,24 @@
 // 2. Wave streams (jv_rstream_build / _export).  Per direction (factor,
 //    forward, backward): rows of each region in (level, row) order = local
 //    slots; consecutive rows of one level in waves of <= threads rows; every
-//    wave is a 16-byte aligned structure-of-arrays block of int32 words
-//        [cnt, slot0, K, NP, row[cnt], p0[cnt], meta[cnt], ref[K][cnt],
-//         pslot[NP]]
+//    wave is a 16-byte aligned block of int32 words
+//        [cnt, slot0, K, NP | rec[cnt] | xref[K - 4][cnt] | pslot[NP]]
+//    with one 32-byte record per row,
+//        rec = {ref0, ref1, ref2, ref3, p0, row, meta, me},
 //    K = most dependencies of a row in the wave, meta = ndep | pub << 6 |
-//    umask << 7 (factor), ref >= 0: slot in the region's ring, < 0:
-//    -(1 + j), the wave's j-th remote dependency, mailbox slot pslot[j];
-//    The factor's u(c_k, r) come with the packed values.  The wave's dynamic block holds
-//    vals[NV][cnt] (matrix values, right-hand side; gathered at run time)
-//    and NP 16-byte mailbox packets.  Static blocks are bulk-copied (TMA) S waves ahead into
-//    a shared-memory ring, dynamic blocks gathered D waves ahead; ring
-//    offsets are placed here by simulating both FIFO rings.
+//    umask << 7 (factor).  A ref is the BYTE OFFSET in the CTA's shared
+//    memory of the dependency's value: a slot of the region's value ring, an
+//    entry of the wave's decoded remote values (written by the prober warp
+//    from the mailbox packets pslot[j]), or the constant 1.0 for the unused
+//    refs of a row with fewer than 4 dependencies — the kernel reads every
+//    ref with one load and no case distinction.  `me` is the offset of the
+//    row's own ring slot.  Dependencies beyond the fourth are in xref.
+//    The factor's u(c_k, r) come with the packed values.  The wave's dynamic
+//    block holds vals[NV][cnt] (matrix values), the per-call vector, NP
+//    16-byte mailbox packets and NP decoded doubles.  Static blocks are
+//    bulk-copied (TMA) S waves ahead into a shared-memory ring, dynamic
+//    blocks D waves ahead; ring offsets are placed here by simulating both
+//    FIFO rings, and the remote refs are patched once the rings are placed.
 #include "../../include/jv.h"
 
 #include <algorithm>
@@ -354,6 +361,9 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
     const int32_t wv = wave_of_slot[slot_of[r]];
     return wave_first[wv] + wave_cnt[wv] - 1 - slot_of[c] < SC;
   };
+  // shared-memory byte offsets the refs point to (region.cu's layout)
+  const int32_t kOneOff = 144;                             // the constant 1.0
+  const int32_t slot_base = 256 + 32 * R->max_waves;       // value ring
   auto emit = [&](int32_t SC) {
     std::fill(pub.begin(), pub.end(), 0);
     for (int32_t r = 0; r < n; ++r)
@@ -376,34 +386,38 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
         const int32_t r = slot_row[s0 + i];
         K = std::max(K, dep_hi(r) - dep_lo(r));
       }
-      // SoA block: header, r[], p0[], meta[], ref[K][], pslot[]
-      ref.assign((size_t)K * cnt, 0);
+      // block: header, 32-byte records, xref[K - 4][], pslot[]
+      const int32_t KX = std::max(K - 4, 0);
+      ref.assign((size_t)KX * cnt, kOneOff);
       pslot.clear();
       const size_t base = W.size();
       goff[w] = (int32_t)(base / 4);
-      W.resize(base + 4 + (size_t)3 * cnt, 0);
+      W.resize(base + 4 + (size_t)8 * cnt, 0);
       for (int32_t i = 0; i < cnt; ++i) {
         const int32_t r = slot_row[s0 + i];
         const int32_t lo = dep_lo(r), hi = dep_hi(r), nd = hi - lo;
         int32_t nrem = 0;
+        int32_t* rec = &W[base + 4 + (size_t)8 * i];
+        for (int32_t k = 0; k < 4; ++k) rec[k] = kOneOff;
         for (int32_t p = lo; p < hi; ++p) {
           const int32_t c = col[p];
           int32_t v;
           if (local(r, c, SC)) {
-            v = (slot_of[c] - reg_ptr[g]) % SC;
+            v = slot_base + 8 * ((slot_of[c] - reg_ptr[g]) % SC);
           } else {
-            v = -(1 + (int32_t)pslot.size());
+            v = -(1 + (int32_t)pslot.size());   // patched after ring placement
             pslot.push_back(c);   // mailbox slot = row (dense: 8 packets per 128-byte line)
             ++nrem;
           }
-          ref[(size_t)(p - lo) * cnt + i] = v;
+          if (p - lo < 4) rec[p - lo] = v;
+          else ref[(size_t)(p - lo - 4) * cnt + i] = v;
         }
         R->ndeps_remote += nrem;
         R->nrows_remote += nrem > 0;
-        W[base + 4 + i] = r;
-        W[base + 4 + cnt + i] = kind == 2 ? diag[r] : rs[r];
-        W[base + 4 + 2 * cnt + i] =
-            nd | (pub[r] ? 1 << 6 : 0) | (kind == 0 ? umask[r] << 7 : 0);
+        rec[4] = kind == 2 ? diag[r] : rs[r];
+        rec[5] = r;
+        rec[6] = nd | (pub[r] ? 1 << 6 : 0) | (kind == 0 ? umask[r] << 7 : 0);
+        rec[7] = slot_base + 8 * ((s0 - reg_ptr[g] + i) % SC);
       }
       W[base + 0] = cnt;
       W[base + 1] = s0 - reg_ptr[g];
@@ -451,7 +465,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       }
       // then the wave's 16-byte mailbox packets (filled by the prober warp)
       sbytes[w] = (int32_t)(4 * (W.size() - base));
-      dbytes[w] = vb + cb + 16 * (int32_t)pslot.size();
+      dbytes[w] = vb + cb + 16 * (int32_t)pslot.size() + ((8 * (int32_t)pslot.size() + 15) & ~15);
       npk[w] = (int32_t)pslot.size();
       ssz[g].push_back(sbytes[w]);
       dsz[g].push_back(dbytes[w]);
@@ -514,6 +528,21 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       R->table[8 * w + 5] = vbytes[w];
       R->table[8 * w + 6] = coff[w];   // 16-byte units
       R->table[8 * w + 7] = cbytes[w] | (npk[w] << 16);   // | remote packets of the wave
+      // remote refs -> offsets of the wave's decoded values (behind its
+      // packed values, vector and packets in the dynamic ring)
+      const int32_t rem = slot_base + 8 * R->SC + R->CS + dof[k] + vbytes[w] + cbytes[w] +
+                          16 * npk[w];
+      int32_t* blk = &W[(size_t)goff[w] * 4];
+      const int32_t cnt = blk[0], K = blk[2];
+      for (int32_t i = 0; i < cnt; ++i)
+        for (int32_t q = 0; q < 4; ++q) {
+          int32_t& v = blk[4 + 8 * i + q];
+          if (v < 0) v = rem + 8 * (-1 - v);
+        }
+      for (int32_t q = 0; q < std::max(K - 4, 0) * cnt; ++q) {
+        int32_t& v = blk[4 + 8 * cnt + q];
+        if (v < 0) v = rem + 8 * (-1 - v);
+      }
     }
   }
   sizes[0] = 4 * (int64_t)W.size();

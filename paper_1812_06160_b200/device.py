@@ -124,6 +124,7 @@ def _registered(a):
     return True
 
 
+_REGION_D_CAP = int(os.environ.get("JV_REGION_D", "99"))   # diagnostics: shallower prefetch
 STREAM_MIN_BYTES = 32 << 20    # streamed factor_serial above this many value bytes
 
 
@@ -855,7 +856,8 @@ class DevIlu:
             before_kernel()
         _lib.call("jv_region_run", kind, rp["nreg"], rp["max_rows"], ptr(rp["words"]),
                   ptr(rp["table"]),
-                  ptr(rp["reg_wave"]), rp["slot_ring"], rp["max_waves"], rp["S"], rp["D"],
+                  ptr(rp["reg_wave"]), rp["slot_ring"], rp["max_waves"], rp["S"],
+                  min(rp["D"], _REGION_D_CAP),
                   rp["CS"], rp["CD"], ptr(self.val), ptr(rp["pack"]), ptr(rp["vpack"]),
                   ptr(out), ptr(self.norms),
                   self.tau, ptr(box.buf), box.next_epoch(), ptr(self.err), stream())

@@ -30,6 +30,17 @@ def row_inf_norms(factors: IluFactors) -> np.ndarray:
     return dv.host_f64(d.norms, factors.n)
 
 
+def _host_values(factors: IluFactors) -> np.ndarray:
+    """The caller's value array as contiguous float64 (replaced in the
+    factors only when it is not already), without counting as a read."""
+    host = factors._host()
+    if not (isinstance(host, np.ndarray) and host.dtype == np.float64
+            and host.flags.c_contiguous):
+        factors.val = np.ascontiguousarray(host, dtype=np.float64)
+        host = factors._host()
+    return host
+
+
 def _run(factors: IluFactors, lo=0, hi=None, ready_below=0, keep_after_bad=False) -> int:
     d = factors.upload_values()
     bad = d.factor(lo, hi, ready_below)
@@ -38,8 +49,12 @@ def _run(factors: IluFactors, lo=0, hi=None, ready_below=0, keep_after_bad=False
         # the reference stops at the first zero pivot: rows after it keep
         # their input values, which the host array still holds
         n_out = int(factors.pattern.row_start[bad + 1])
-    factors.val = np.ascontiguousarray(factors.val, dtype=np.float64)
-    dv.download_f64(factors.val, d.val, n_out)
+    host = _host_values(factors)
+    dv.download_f64(host, d.val, n_out)
+    if n_out == factors.pattern.nnz:
+        factors._synced()   # host and device hold the same factors now
+    else:
+        factors._dirty = True
     return bad
 
 
@@ -51,27 +66,33 @@ def factor_serial(factors: IluFactors) -> None:
     matches the reference's."""
     if factors.n == 0:
         return
-    factors.val = np.ascontiguousarray(factors.val, dtype=np.float64)
-    if factors.pattern.nnz * 8 >= dv.STREAM_MIN_BYTES and dv.pinned_host(factors.val):
+    host = _host_values(factors)
+    if (factors.pattern.nnz * 8 >= dv.STREAM_MIN_BYTES and not factors.device_is_current()
+            and dv.pinned_host(host)):
         # large page-locked host values: upload, factorization and download
         # overlap chunk by chunk (DevIlu.factor_streamed)
         d = factors.device()
-        bad = d.factor_streamed(factors.val)
+        bad = d.factor_streamed(host)
         d.holder = factors
+        if bad < 0:
+            factors._synced()
+        else:
+            factors._dirty = True
     else:
         bad = _run(factors, keep_after_bad=True)
     if bad >= 0:
         raise ZeroPivotError(int(bad))
 
 
-def _row_range(rows: np.ndarray, n: int):
-    """[lo, hi) when `rows` is exactly a contiguous index range."""
-    if rows.size == 0:
-        return 0, 0
-    lo, hi = int(rows.min()), int(rows.max()) + 1
-    if hi - lo == rows.size and np.unique(rows).size == rows.size:
-        return lo, hi
-    return None
+def _row_runs(rows: np.ndarray):
+    """The maximal runs [lo, hi) of consecutive indices in the row set."""
+    r = np.unique(rows)
+    if r.size == 0:
+        return []
+    brk = np.flatnonzero(np.diff(r) != 1)
+    los = np.concatenate(([r[0]], r[brk + 1]))
+    his = np.concatenate((r[brk] + 1, [r[-1] + 1]))
+    return [(int(a), int(b)) for a, b in zip(los, his)]
 
 
 def factor_parallel_upper(factors: IluFactors, schedule) -> None:
@@ -79,14 +100,26 @@ def factor_parallel_upper(factors: IluFactors, schedule) -> None:
 
     The point-to-point waits of `schedule` are not needed on the GPU: each
     row awaits its own pivots through the mailbox, in any order; only the
-    row set matters."""
+    row set matters.  Rows outside the set are read as they are (the
+    reference's kernels never wait for them either): the set is factored
+    run by run of consecutive rows in ascending order, each launch taking
+    everything below its run as final — one launch for the usual upper
+    block [0, n_upper)."""
     rows = np.asarray(schedule.order, dtype=np.int64)
     if factors.n == 0 or rows.size == 0:
         return
-    rng = _row_range(rows, factors.n)
-    if rng is None:
-        raise NotImplementedError("factor_parallel_upper: schedule rows must form an index range")
-    lo, hi = rng
-    bad = _run(factors, lo, hi, ready_below=lo)
+    runs = _row_runs(rows)
+    if len(runs) == 1:
+        lo, hi = runs[0]
+        bad = _run(factors, lo, hi, ready_below=lo)
+    else:
+        d = factors.upload_values()
+        bad = -1
+        for lo, hi in runs:
+            b = d.factor(lo, hi, lo)
+            if b >= 0 and bad < 0:
+                bad = b
+        dv.download_f64(_host_values(factors), d.val, factors.pattern.nnz)
+        factors._synced()
     if bad >= 0:
         raise ZeroPivotError(int(bad))

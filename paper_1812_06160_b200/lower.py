@@ -210,8 +210,10 @@ def _factor_tail(factors: IluFactors, n_upper: int) -> None:
 
     d = factors.upload_values()
     bad = d.factor_tail(n_upper)
-    factors.val = np.ascontiguousarray(factors.val, dtype=np.float64)
-    dv.download_f64(factors.val, d.val, factors.pattern.nnz)
+    from .factor import _host_values
+
+    dv.download_f64(_host_values(factors), d.val, factors.pattern.nnz)
+    factors._synced()
     if bad >= 0:
         raise ZeroPivotError(int(bad))
 

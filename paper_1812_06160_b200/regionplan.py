@@ -112,21 +112,45 @@ def _build(sweep, row_start, col, diag, region_of, nreg, smem_budget, tau, threa
                       int(sizes[12]))
 
 
+ONE_OFF = 144   # shared-memory offset of the constant 1.0 (region.cu)
+
+
 def records(ws: WaveStream, w):
-    """(slot0, [record dicts]) of wave w (host decoding, for tests/tools)."""
+    """(slot0, [record dicts]) of wave w (host decoding, for tests/tools).
+    refs are translated back from shared-memory byte offsets: >= 0 a slot of
+    the region's value ring, < 0: -(1 + j), the wave's j-th remote
+    dependency (mailbox slot pslot[j])."""
     base = int(ws.table[w, 0]) * 4
     blk = ws.words[base:base + int(ws.table[w, 1]) // 4]
     cnt, slot0, K, NP = (int(x) for x in blk[:4])
-    row, p0, meta = blk[4:4 + cnt], blk[4 + cnt:4 + 2 * cnt], blk[4 + 2 * cnt:4 + 3 * cnt]
-    ref = blk[4 + 3 * cnt:4 + (3 + K) * cnt].reshape(K, cnt)
-    off = 4 + (3 + K) * cnt
+    rec = blk[4:4 + 8 * cnt].reshape(cnt, 8)
+    kx = max(K - 4, 0)
+    xref = blk[4 + 8 * cnt:4 + (8 + kx) * cnt].reshape(kx, cnt)
+    off = 4 + (8 + kx) * cnt
     pslot = blk[off:off + NP]
+    slot_base = 256 + 32 * ws.max_waves
+    rem_base = slot_base + 8 * ws.slot_ring + ws.CS + int(ws.table[w, 3]) + int(ws.table[w, 5]) + \
+        (int(ws.table[w, 7]) & 0xFFFF) + 16 * NP
+
+    def back(off):
+        off = int(off)
+        if slot_base <= off < slot_base + 8 * ws.slot_ring:
+            assert (off - slot_base) % 8 == 0
+            return (off - slot_base) // 8
+        j = (off - rem_base) // 8
+        assert (off - rem_base) % 8 == 0 and 0 <= j < NP, (off, rem_base, NP)
+        return -1 - j
+
     out = []
     for i in range(cnt):
-        nd = int(meta[i]) & 63
-        refs = ref[:nd, i]
-        out.append(dict(r=int(row[i]), p0=int(p0[i]), nd=nd, pub=(int(meta[i]) >> 6) & 1,
-                        umask=(int(meta[i]) >> 7) & 15, refs=refs,
+        meta = int(rec[i, 6])
+        nd = meta & 63
+        raw = [rec[i, k] if k < 4 else xref[k - 4, i] for k in range(nd)]
+        assert all(int(rec[i, k]) == ONE_OFF for k in range(nd, 4))
+        assert int(rec[i, 7]) == slot_base + 8 * ((slot0 + i) % ws.slot_ring)
+        refs = np.array([back(x) for x in raw], np.int64)
+        out.append(dict(r=int(rec[i, 5]), p0=int(rec[i, 4]), nd=nd, pub=(meta >> 6) & 1,
+                        umask=(meta >> 7) & 15, refs=refs,
                         rsl=np.array([pslot[-1 - int(x)] for x in refs if x < 0], np.int64),
                         K=K, cnt=cnt, NP=NP))
     return slot0, out

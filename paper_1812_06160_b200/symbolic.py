@@ -11,6 +11,7 @@ the diagonal.
 from __future__ import annotations
 
 import ctypes
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -56,10 +57,10 @@ class IluFactors:
         return self.val[self.pattern.row_start[i]:self.pattern.row_start[i + 1]]
 
     def copy(self) -> "IluFactors":
-        return IluFactors(self.n, self.pattern, self.val.copy(), self.diag_pos, self.perm,
+        return IluFactors(self.n, self.pattern, self._val.copy(), self.diag_pos, self.perm,
                           self.drop_tol, self.milu, self._dev)
 
-    # device mirror of the structure (values are uploaded per call) ------
+    # device mirror of the structure ---------------------------------------
     def device(self) -> dv.DevIlu:
         key = (id(self.pattern.row_start), id(self.pattern.col), id(self.diag_pos), self.n)
         if self._dev is None or self._dev[0] != key:
@@ -75,13 +76,52 @@ class IluFactors:
         d.milu = bool(self.milu)
         return d
 
+    # Host values and their device copy.  `val` is the caller's numpy array,
+    # as in the reference; the device copy is reused across calls only while
+    # the package can prove the host array is unchanged: nobody has read the
+    # `val` attribute since the last transfer (a read hands out a reference
+    # the caller may write through) and nobody else holds a reference to the
+    # array (a kept alias or view).  The reference's Krylov pattern
+    # `precond = lambda r: apply_preconditioner(factors, r)` (pipeline.py:300)
+    # then moves only the vector per call instead of all factor values.
+    def _host(self) -> np.ndarray:
+        """The host value array, without marking it as handed out."""
+        return self._val
+
+    def _synced(self) -> None:
+        """Host array and device copy hold the same values as of now."""
+        self._dirty = False
+
+    def device_is_current(self) -> bool:
+        d = self._dev[1] if self._dev is not None else None
+        return (d is not None and d.holder is self and not self._dirty
+                and sys.getrefcount(self._val) <= 2)
+
     def upload_values(self) -> dv.DevIlu:
         d = self.device()
+        if self.device_is_current():
+            return d
         if self.pattern.nnz:
-            dv.upload_f64(d.val, self.val)
+            dv.upload_f64(d.val, self._val)
         d.values_changed()
         d.holder = self
+        self._dirty = False
         return d
+
+
+def _get_val(self) -> np.ndarray:
+    self._dirty = True
+    return self._val
+
+
+def _set_val(self, v) -> None:
+    self._val = v
+    self._dirty = True
+
+
+# (a property over the dataclass field: the generated __init__ assigns
+# through the setter)
+IluFactors.val = property(_get_val, _set_val)
 
 
 def _dev_pattern(p: SparsityPattern) -> dv.DevCsr:

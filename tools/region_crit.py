@@ -37,9 +37,11 @@ buf = torch.zeros(16 * nw, dtype=torch.int64, device="cuda")
 fn()
 torch.cuda.synchronize()
 _lib.call("jv_set_trace", dv.ptr(buf), nw)
+_lib.call("jv_set_region_flags", int(os.environ.get("JV_RFLAGS", "0")))
 fn()
 torch.cuda.synchronize()
 _lib.call("jv_set_trace", None, 0)
+_lib.call("jv_set_region_flags", 0)
 tr = buf.cpu().numpy().reshape(nw, 16)
 g = tr[:, 0:8].astype(np.float64)
 c = tr[:, 8:16]
@@ -62,6 +64,10 @@ else:
         lev[r] = lev[l].max() + 1 if l.size else 0
 wl = np.array([lev[words[int(table[w, 0]) * 4 + 4]] for w in range(nw)])
 L = wl.max() + 1
+if os.environ.get("JV_CRIT_DUMP"):
+    np.savez_compressed(os.environ["JV_CRIT_DUMP"], g=tr[:, 0:8], c=c, wl=wl, rw=rw,
+                        cnt=np.array([words[int(table[w, 0]) * 4] for w in range(nw)]),
+                        npk=table[:, 7] >> 16)
 crit = np.array([np.argmax(np.where(wl == l, end, -1)) for l in range(L)])
 tl = end[crit]
 dt = np.diff(np.concatenate([[0.0], tl]))
