@@ -43,6 +43,7 @@ namespace jvr {
 
 constexpr int kThreads = 512;   // rows per wave (compute threads)
 constexpr int kNB = 16;   // static-block mbarriers in the ring (S + 1 <= kNB)
+constexpr int kTab = 3;   // int4 entries per wave in the shared-memory table
 constexpr int kL2 = 12;   // waves of L2 bulk prefetch ahead of the gathers (24 measured equal)
 
 struct RArgs {
@@ -105,7 +106,7 @@ struct Wave {
 constexpr int kOneOff = 144;   // shared-memory offset of the constant 1.0
 constexpr int kCompute = 512;
 constexpr int kProbers = 4;             // prober warps; warp p owns the waves w with w % kProbers == p
-constexpr int kExtra = 32 + 32 * kProbers;   // a producer warp (one lane) and the prober warps
+constexpr int kExtra = 64 + 32 * kProbers;   // a producer warp (one lane), a waiter warp and the prober warps
 constexpr int kBlock = kCompute + kExtra;
 constexpr int kWin = 4;                 // prober window (waves; 16 and 2 measured slower on c2)
 
@@ -151,12 +152,18 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
   int* done = reinterpret_cast<int*>(rsm + 8 * kNB);          // waves finished
   int* issued = done + 2;   // waves whose blocks the producer has issued
   int* probed = done + 8;   // [kProbers] per prober warp: its waves below this are released
-  int4* tab = reinterpret_cast<int4*>(rsm + 256);             // 2 per wave
-  unsigned char* sring = rsm + 256 + 32 * A.max_waves + 8 * A.SC;
+  int4* tab = reinterpret_cast<int4*>(rsm + 256);             // kTab per wave: the two table
+                                                              // entries and the block header
+  unsigned char* sring = rsm + 256 + 16 * kTab * A.max_waves + 8 * A.SC;
   unsigned char* dring = sring + A.CS;
   const int w0 = A.reg_wave[blockIdx.x];
   const int nw = A.reg_wave[blockIdx.x + 1] - w0;
-  for (int i = tid; i < 2 * nw; i += blockDim.x) tab[i] = A.table[2 * w0 + i];
+  for (int i = tid; i < nw; i += blockDim.x) {
+    const int4 t = A.table[2 * (w0 + i)];
+    tab[kTab * i] = t;
+    tab[kTab * i + 1] = A.table[2 * (w0 + i) + 1];
+    tab[kTab * i + 2] = A.words[t.x];   // {cnt, slot0, K, NP}: read before the block lands
+  }
   if (tid == 0) {
     for (int b = 0; b < kNB; ++b) bar_init(&bar[b], 1);
     *done = 0;
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
   const bool tau = KIND == 0 && A.tau > 0.0;
   const unsigned flags = jv::g_region_flags;
 
-  if (tid >= kCompute + 32) {
+  if (tid >= kCompute + 64) {
     // -------------------------------------------------------------- prober
     // Fetches the mailbox packets of the remote dependencies of the next
     // kWin waves, round after round: each round copies every still-stale
@@ -187,14 +194,14 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
     // takes about as long as three waves of compute and was the pacemaker
     // of every region but the first (measured: a stall every third wave).
     const int lane = tid & 31;
-    const int pw = (tid - kCompute - 32) >> 5;
+    const int pw = (tid - kCompute - 64) >> 5;
     constexpr int P = kProbers;
     int* const myprobed = probed + pw;
     auto pkts = [&](int x) -> unsigned char* {
-      const int4 v = tab[2 * x + 1];
-      return dring + tab[2 * x].w + v.y + (v.w & 0xffff);
+      const int4 v = tab[kTab * x + 1];
+      return dring + tab[kTab * x].w + v.y + (v.w & 0xffff);
     };
-    auto np = [&](int x) { return tab[2 * x + 1].w >> 16; };
+    auto np = [&](int x) { return tab[kTab * x + 1].w >> 16; };
     auto fresh = [&](const unsigned char* p) {
       const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(p);
       return (uint32_t)(q.x >> 32) == A.epoch && (uint32_t)(q.y >> 32) == A.epoch;
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
       while (hi < nw && hi < lo + kWin * P) {
         if (np(hi) > 0) {
           if (hi >= iss || !bar_test(&bar[hi % kNB], (uint32_t)((hi / kNB) & 1))) break;
-          const Wave X(sring + tab[2 * hi].z);
+          const Wave X(sring + tab[kTab * hi].z);
           unsigned char* pk = pkts(hi);
           if (!(flags & 8))
             for (int j = lane; j < X.NP; j += 32) {
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
       // one round: copy every stale packet of the window
       for (int x = lo; x < hi0; x += P) {
         if (np(x) == 0) continue;
-        const Wave X(sring + tab[2 * x].z);
+        const Wave X(sring + tab[kTab * x].z);
         unsigned char* pk = pkts(x);
         for (int j = lane; j < X.NP; j += 32)
           if (!fresh(pk + 16 * j) && !(flags & 8)) {
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
       const int lo0 = lo;
       while (lo < hi) {
         if (np(lo) > 0) {
-          const Wave X(sring + tab[2 * lo].z);
+          const Wave X(sring + tab[kTab * lo].z);
           const unsigned char* pk = pkts(lo);
           bool ok = true;
           for (int j = lane; j < X.NP; j += 32) ok = ok && ((flags & 8) || fresh(pk + 16 * j));
@@ -280,11 +287,34 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
     }
     return;
   }
+  if (tid >= kCompute + 32) {
+    // -------------------------------------------------------------- waiter
+    // Takes part in the compute warps' barrier so that they never touch an
+    // mbarrier: in front of the barrier that ends wave w its lane 0 waits
+    // for the blocks of wave w + 2 (when the compute warps start wave w + 1
+    // and load the operands of wave w + 2, those have landed); behind it,
+    // it publishes the progress counter the producer reads.
+    const bool lead = tid == kCompute + 32;
+    if (lead) {
+      bar_wait(&bar[0], 0);
+      if (nw > 1) bar_wait(&bar[1 % kNB], 0);
+    }
+    __syncwarp();
+    asm volatile("bar.sync 1, %0;" ::"n"(kCompute + 32) : "memory");
+    for (int w = 0; w < nw; ++w) {
+      if (lead && w + 2 < nw) bar_wait(&bar[(w + 2) % kNB], (uint32_t)(((w + 2) / kNB) & 1));
+      __syncwarp();
+      asm volatile("bar.sync 1, %0;" ::"n"(kCompute + 32) : "memory");
+      if (lead)
+        asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(done)), "r"(w + 1) : "memory");
+    }
+    return;
+  }
   if (tid >= kCompute) {
     // ------------------------------------------------------------ producer
     if (tid != kCompute) return;
     auto prefetch = [&](int x) {
-      const int4 t2 = tab[2 * x], v2 = tab[2 * x + 1];
+      const int4 t2 = tab[kTab * x], v2 = tab[kTab * x + 1];
       l2_prefetch_bulk(A.words + t2.x, (uint32_t)t2.y);
       if (v2.y > 0) l2_prefetch_bulk(A.pack + 2 * (int64_t)v2.x, (uint32_t)v2.y);
       if (v2.w & 0xffff) l2_prefetch_bulk(A.vpack + 2 * (int64_t)v2.z, (uint32_t)(v2.w & 0xffff));
@@ -297,7 +327,7 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
       // ring blocks of wave x may overlap those of wave x - D - 1
       while (ld_volatile_shared(done) < x - D) __nanosleep(20);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int4 t = tab[2 * x], v = tab[2 * x + 1];
+      const int4 t = tab[kTab * x], v = tab[kTab * x + 1];
       uint64_t* b = &bar[x % kNB];
       const bool skip = flags & 4;   // diagnostic: no value copies (wrong results)
       const int cb = v.w & 0xffff;
@@ -343,25 +373,37 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
     const int32_t* xref;
     const double* vals;
   };
-  auto fetch = [&](int w, Ops& s) {
-    bar_wait(&bar[w % kNB], (uint32_t)((w / kNB) & 1));
-    const int4 t = lds128(tab_off + 32 * w);
-    const int4 tv = lds128(tab_off + 32 * w + 16);
-    const uint32_t blk = sring_off + t.z;
-    const int4 hd = lds128(blk);   // cnt, slot0, K, NP
-    const int cnt = hd.x, K = hd.z;
+  struct Tab {            // a wave's table entries (static shared memory)
+    int so, dof, vbytes, cnt, K, np;
+  };
+  auto load_tab = [&](int w, Tab& t) {
+    const int4 a0 = lds128(tab_off + 16 * kTab * w);
+    const int4 a1 = lds128(tab_off + 16 * kTab * w + 16);
+    const int4 hd = lds128(tab_off + 16 * kTab * w + 32);
+    t.so = a0.z;
+    t.dof = a0.w;
+    t.vbytes = a1.y;
+    t.cnt = hd.x;
+    t.K = hd.z;
+    t.np = hd.w;
+  };
+  // operands of a wave whose blocks have landed (the producer warp saw to
+  // it before the last barrier): loads only, every address from registers
+  auto fetch = [&](const Tab& t, Ops& s) {
+    const uint32_t blk = sring_off + t.so;
+    const int cnt = t.cnt, K = t.K;
     s.cnt = cnt;
     s.K = K;
-    s.np = hd.w;
+    s.np = t.np;
     s.xref = reinterpret_cast<const int32_t*>(rsm + blk) + 4 + 8 * cnt;
-    s.vals = reinterpret_cast<const double*>(rsm + dring_off + t.w);
+    s.vals = reinterpret_cast<const double*>(rsm + dring_off + t.dof);
     // threads beyond the wave take its last row's operands
     const int i = min(tid, cnt - 1);
     s.r0 = lds128(blk + 16 + 32 * i);
     s.r1 = lds128(blk + 32 + 32 * i);
-    const uint32_t vp = dring_off + t.w + 8 * i;   // vals[k][i] at vp + 8 * k * cnt
+    const uint32_t vp = dring_off + t.dof + 8 * i;   // vals[k][i] at vp + 8 * k * cnt
     const uint32_t c8 = 8 * cnt;
-    const uint32_t vec = dring_off + t.w + tv.y + 8 * i;
+    const uint32_t vec = dring_off + t.dof + t.vbytes + 8 * i;
     if (KIND == 0) {
       // a_k, a_rr, u_k in vals[2K + 1][cnt]; the pack holds +0.0 for the
       // entries of rows with fewer than K pivots
@@ -389,7 +431,7 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
   const jv::Trace T = jv::trace_begin();
   const bool tracing = T.p != nullptr && tid == 0;
 #endif
-  auto step = [&](int w, const Ops& cur, Ops& nxt) {
+  auto step = [&](int w, const Ops& cur, Ops& nxt, const Tab& tn, Tab& tnn) {
     // the prober has released this wave's remote dependencies (a wave
     // without any passes straight through)
     if (cur.np > 0) {
@@ -403,12 +445,10 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
     dv[2] = lds64(cur.r0.z);
     dv[3] = lds64(cur.r0.w);
     // the next wave's operands, in flight during this wave's arithmetic
-    // (after the last wave: that wave again, its blocks are still there)
-#if (JV_RDIAG & 1)
-    nxt = cur;
-#else
-    fetch(min(w + 1, nw - 1), nxt);
-#endif
+    // (after the last wave: that wave again, its blocks are still there),
+    // and the table entries of the wave after it
+    fetch(tn, nxt);
+    load_tab(min(w + 2, nw - 1), tnn);
     const int cnt = cur.cnt, K = cur.K;
     const bool active = tid < cnt;
     const int meta = cur.r1.z, nd = meta & 63, row = cur.r1.y, p0 = cur.r1.x;
@@ -423,15 +463,7 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
       // pivots beyond the row's own: a = +0.0 (K > k >= nd) or a copy of an
       // earlier operand (k >= K), never used: umask and the stores are per nd
       double l[4];
-      {
-        double a3[3] = {cur.a[0], cur.a[1], cur.a[2]}, d3[3] = {dv[0], dv[1], dv[2]}, l3[3];
-        jv::ddiv_batch<3>(a3, d3, l3, nd);
-        l[0] = l3[0];
-        l[1] = l3[1];
-        l[2] = l3[2];
-        l[3] = 0.0;
-        if (K > 3) l[3] = jv::ddiv(cur.a[3], dv[3]);
-      }
+      jv::ddiv_batch<4>(cur.a, dv, l, nd);   // (four interleaved chains cost the latency of one)
       const double thresh = jv::dmul(tauv, cur.rhs);
       double d = cur.dg;
       const int umask = (meta >> 7) & 15;
@@ -474,24 +506,28 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
     if (pub) jv::mbox_put(mbox, row, res, epoch);
 #endif
 #if !(JV_RDIAG & 8)
-    asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kCompute + 32) : "memory");
 #endif
-    if (tid == 0) {
-      asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(done)), "r"(w + 1) : "memory");
 #ifdef JV_REGION_TRACE
-      if (tracing) jv::trace_clock(T, w0 + w, 7);
-#endif
+    if (tracing) {
+      if (flags & 16) jv::trace_clock(T, w0 + w, 7);   // 16: clock only (no globaltimer read)
+      else jv::trace_mark(T, w0 + w, 7);
     }
+#endif
   };
+  asm volatile("bar.sync 1, %0;" ::"n"(kCompute + 32) : "memory");   // blocks 0 and 1 have landed
   if (nw > 0) {
     Ops oa, ob;
-    fetch(0, oa);
+    Tab ta, tb;
+    load_tab(0, ta);
+    load_tab(min(1, nw - 1), tb);
+    fetch(ta, oa);
     int w = 0;
     for (; w + 1 < nw; w += 2) {
-      step(w, oa, ob);
-      step(w + 1, ob, oa);
+      step(w, oa, ob, tb, ta);       // consumes the entries of w + 1, loads those of w + 2
+      step(w + 1, ob, oa, ta, tb);
     }
-    if (w < nw) step(w, oa, ob);
+    if (w < nw) step(w, oa, ob, tb, ta);
   }
 }
 
@@ -581,7 +617,7 @@ extern "C" int jv_set_region_flags(unsigned flags) {
 }
 
 extern "C" int64_t jv_region_smem_fixed(int32_t slot_ring, int32_t max_waves) {
-  return 256 + 32 * (int64_t)max_waves + 8 * (int64_t)slot_ring;
+  return 256 + 16 * jvr::kTab * (int64_t)max_waves + 8 * (int64_t)slot_ring;
 }
 
 extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const void* words,
@@ -590,7 +626,7 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const
                              int32_t S, int32_t D, int32_t CS, int32_t CD, double* val,
                              const double* pack, const double* vpack, double* out, const double* norms, double tau,
                              uint64_t* mbox, uint32_t epoch, int32_t* err_row, void* stream) {
-  if (kind < 0 || kind > 2 || nreg < 1 || epoch == 0 || D < 1 || D > 12 || S < D ||
+  if (kind < 0 || kind > 2 || nreg < 1 || epoch == 0 || D < 2 || D > 12 || S < D ||
       slot_ring < 1 || (slot_ring & (slot_ring - 1)) ||
       S + 1 > jvr::kNB) {
     jvh::set_error("jv_region_run: bad argument (kind=%d nreg=%d S=%d D=%d)", kind, nreg, S, D);

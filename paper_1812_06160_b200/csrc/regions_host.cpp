@@ -363,7 +363,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   };
   // shared-memory byte offsets the refs point to (region.cu's layout)
   const int32_t kOneOff = 144;                             // the constant 1.0
-  const int32_t slot_base = 256 + 32 * R->max_waves;       // value ring
+  const int32_t slot_base = 256 + 48 * R->max_waves;       // value ring
   auto emit = [&](int32_t SC) {
     std::fill(pub.begin(), pub.end(), 0);
     for (int32_t r = 0; r < n; ++r)
@@ -476,10 +476,10 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   // in-region dependencies through the mailbox, where the D-wave prefetch
   // finds them long published)
   auto fit = [&](int64_t SC, int32_t& D_, int32_t& cs_, int32_t& cd_) {
-    const int64_t fixed = 512 + 32 * (int64_t)R->max_waves + 8 * SC;
+    const int64_t fixed = 512 + 48 * (int64_t)R->max_waves + 8 * SC;
     const int64_t ring = (smem_budget - fixed) & ~(int64_t)15;
     if (ring < 1024) return false;
-    for (int D = 8; D >= 1; --D) {
+    for (int D = 8; D >= 2; --D) {   // (the kernel's producer needs two waves of slack)
       const int32_t cd = min_cap(dsz, D, (int32_t)ring);
       if (cd < 0) continue;
       const int32_t cs = min_cap(ssz, D, (int32_t)(ring - cd));

@@ -62,7 +62,7 @@ else:
     for r in range(n):
         l = col[rs[r]:diag[r]]
         lev[r] = lev[l].max() + 1 if l.size else 0
-wl = np.array([lev[words[int(table[w, 0]) * 4 + 4]] for w in range(nw)])
+wl = np.array([lev[words[int(table[w, 0]) * 4 + 4 + 5]] for w in range(nw)])   # first record's row
 L = wl.max() + 1
 if os.environ.get("JV_CRIT_DUMP"):
     np.savez_compressed(os.environ["JV_CRIT_DUMP"], g=tr[:, 0:8], c=c, wl=wl, rw=rw,
