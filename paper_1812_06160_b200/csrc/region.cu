@@ -179,20 +179,13 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
 
   if (tid >= kCompute + 64) {
     // -------------------------------------------------------------- prober
-    // Fetches the mailbox packets of the remote dependencies of the next
-    // kWin waves, round after round: each round copies every still-stale
-    // packet of the window (cp.async, all in flight together, one round
-    // trip), then checks the epochs in shared memory; the window's first
-    // wave is released to the compute warps (`probed`) once all of its
-    // packets are current.  Decoupled from the compute warps' barrier
-    // cadence, so a value published upstream reaches a waiting wave within
-    // about one round trip, and values published earlier cost nothing.
-    // Several prober warps share the work: warp p owns the waves w with
-    // w % kProbers == p (its own window, its own release counter), so their
-    // round trips overlap and the window reaches kWin * kProbers waves
-    // ahead — a single warp's round (fetch, L2 round trip, check, decode)
-    // takes about as long as three waves of compute and was the pacemaker
-    // of every region but the first (measured: a stall every third wave).
+    // The prober warps fetch the remote dependencies of the coming waves
+    // from the mailboxes and release each wave to the compute warps once
+    // all of its values are in.  Warp p owns the waves w with
+    // w % kProbers == p and has its own release counter, so four waves are
+    // in flight and the warps' L2 round trips overlap (a single prober's
+    // round took about as long as three waves of compute and paced every
+    // region but the first: a stall every third wave in the trace).
     const int lane = tid & 31;
     const int pw = (tid - kCompute - 64) >> 5;
     constexpr int P = kProbers;
@@ -202,88 +195,60 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
       return dring + tab[kTab * x].w + v.y + (v.w & 0xffff);
     };
     auto np = [&](int x) { return tab[kTab * x + 1].w >> 16; };
-    auto fresh = [&](const unsigned char* p) {
-      const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(p);
-      return (uint32_t)(q.x >> 32) == A.epoch && (uint32_t)(q.y >> 32) == A.epoch;
-    };
-    int lo = pw, hi = pw;
-    unsigned ns = 0, spins = 0;
     if (flags & 8) {   // diagnostic: no remote waits at all (wrong results)
       if (lane == 0)
         asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(nw + P) : "memory");
       return;
     }
-    while (lo < nw) {
-      // admit waves: one without remote dependencies needs nothing; one with
-      // them once the producer has issued it and its blocks are in (its
-      // packets are then copied unconditionally: the area holds stale data)
-      bool issued_any = false;
-      const int hi0 = hi;
-      const int iss = ld_volatile_shared(issued);
-      while (hi < nw && hi < lo + kWin * P) {
-        if (np(hi) > 0) {
-          if (hi >= iss || !bar_test(&bar[hi % kNB], (uint32_t)((hi / kNB) & 1))) break;
-          const Wave X(sring + tab[kTab * hi].z);
-          unsigned char* pk = pkts(hi);
-          if (!(flags & 8))
-            for (int j = lane; j < X.NP; j += 32) {
-              cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot(j));
-              issued_any = true;
-            }
+    // One wave at a time per warp, one packet per lane: direct 16-byte
+    // relaxed loads from the mailbox (an L2 round trip each), repeated
+    // warp-converged for the lanes whose packet is still stale; a fresh
+    // value goes straight to the wave's decoded-values area.  A value
+    // published upstream is seen within about one L2 round trip.
+    bool hung = false;
+    for (int x = pw; x < nw && !hung; x += P) {
+      if (np(x) > 0) {
+        unsigned spins = 0;
+        while (x >= ld_volatile_shared(issued) ||
+               !bar_test(&bar[x % kNB], (uint32_t)((x / kNB) & 1))) {
+          __nanosleep(32);
+          if (++spins == jv::g_spin_limit) {
+            hung = true;
+            break;
+          }
         }
-        hi += P;
-      }
-      // one round: copy every stale packet of the window
-      for (int x = lo; x < hi0; x += P) {
-        if (np(x) == 0) continue;
+        if (hung) break;
         const Wave X(sring + tab[kTab * x].z);
-        unsigned char* pk = pkts(x);
-        for (int j = lane; j < X.NP; j += 32)
-          if (!fresh(pk + 16 * j) && !(flags & 8)) {
-            cp16(pk + 16 * j, A.mbox + 2 * (int64_t)X.pslot(j));
-            issued_any = true;
-          }
-      }
-      if (__any_sync(full, issued_any))
-        asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
-      __syncwarp();
-      // release the leading waves that are complete
-      const int lo0 = lo;
-      while (lo < hi) {
-        if (np(lo) > 0) {
-          const Wave X(sring + tab[kTab * lo].z);
-          const unsigned char* pk = pkts(lo);
-          bool ok = true;
-          for (int j = lane; j < X.NP; j += 32) ok = ok && ((flags & 8) || fresh(pk + 16 * j));
-          if (!__all_sync(full, ok)) break;
-          // decoded values behind the packets: what the rows' refs point to
-          double* rem = reinterpret_cast<double*>(const_cast<unsigned char*>(pk) + 16 * X.NP);
-          for (int j = lane; j < X.NP; j += 32) {
-            const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(pk + 16 * j);
-            rem[j] = __longlong_as_double((long long)((q.x & 0xffffffffull) | (q.y << 32)));
+        double* rem = reinterpret_cast<double*>(pkts(x) + 16 * X.NP);
+        for (int j0 = 0; j0 < X.NP && !hung; j0 += 32) {
+          const int j = j0 + lane;
+          bool need = j < X.NP;
+          const int64_t slot = need ? X.pslot(j) : 0;
+          spins = 0;
+          while (true) {
+            double v;
+            if (need && jv::mbox_try(A.mbox, slot, A.epoch, v)) {
+              rem[j] = v;
+              need = false;
+            }
+            if (!__any_sync(full, need)) break;
+            if (++spins == jv::g_spin_limit) {
+              hung = true;
+              break;
+            }
           }
         }
-        lo += P;
-      }
-      if (lo != lo0) {
+        if (hung) break;
         __syncwarp();
-        if (lane == 0) {
-          // release: the packets written above are visible to whoever acquires
-          asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(lo) : "memory");
-        }
-        ns = 0;
-        spins = 0;
-      } else if (!__any_sync(full, issued_any)) {
-        // nothing in flight: wait for the producer (or a slow upstream)
-        if (ns) __nanosleep(ns);
-        ns = ns ? min(2 * ns, jv::g_poll_cap) : 16u;
-        if (++spins == jv::g_spin_limit) {
-          atomicExch(&jv::g_hang, 1);
-          if (lane == 0)
-            asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(nw + P) : "memory");
-          break;
-        }
       }
+      // release: the values written above are visible to whoever acquires
+      if (lane == 0)
+        asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(x + P) : "memory");
+    }
+    if (hung) {
+      atomicExch(&jv::g_hang, 1);
+      if (lane == 0)
+        asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(nw + P) : "memory");
     }
     return;
   }
