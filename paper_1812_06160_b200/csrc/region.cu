@@ -105,9 +105,10 @@ struct Wave {
 #endif
 constexpr int kOneOff = 144;   // shared-memory offset of the constant 1.0
 constexpr int kCompute = 512;
-constexpr int kProbers = 4;             // prober warps; warp p owns the waves w with w % kProbers == p
-constexpr int kExtra = 64 + 32 * kProbers;   // a producer warp (one lane), a waiter warp and the prober warps
-constexpr int kBlock = kCompute + kExtra;
+// prober warps (warp p owns the waves w with w % P == p): 8, or 4 beside 512 compute threads
+__host__ __device__ constexpr int probers_for(int nc) { return nc >= 512 ? 4 : 8; }
+// threads beside the compute warps: a producer warp (one lane), a waiter warp, the prober warps
+__host__ __device__ constexpr int extra_for(int nc) { return 64 + 32 * probers_for(nc); }
 constexpr int kWin = 4;                 // prober window (waves; 16 and 2 measured slower on c2)
 
 JV_INLINE void cp16(void* dst, const void* src) {
@@ -143,8 +144,9 @@ JV_INLINE int ld_volatile_shared(const int* p) {
 // compute warps (whose progress it reads from a shared counter before
 // reusing ring space), with L2 bulk prefetches kL2 waves further ahead.
 template <int KIND, int NC = kCompute>
-__global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
-  constexpr int kCompute = NC;   // compute threads: waves of at most NC rows
+__global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) {
+  constexpr int kCompute = NC;
+  constexpr int kProbers = probers_for(NC);   // compute threads: waves of at most NC rows
   extern __shared__ __align__(128) unsigned char rsm[];
   const unsigned full = 0xffffffffu;
   const int tid = threadIdx.x;
@@ -206,7 +208,13 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
     // value goes straight to the wave's decoded-values area.  A value
     // published upstream is seen within about one L2 round trip.
     bool hung = false;
+#ifdef JV_REGION_TRACE
+    const jv::Trace PT = jv::trace_begin();
+#endif
     for (int x = pw; x < nw && !hung; x += P) {
+#ifdef JV_REGION_TRACE
+      if (lane == 0) jv::trace_word(PT, w0 + x, 3, clock64());   // prober turns to wave x
+#endif
       if (np(x) > 0) {
         unsigned spins = 0;
         while (x >= ld_volatile_shared(issued) ||
@@ -218,6 +226,9 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
           }
         }
         if (hung) break;
+#ifdef JV_REGION_TRACE
+        if (lane == 0) jv::trace_word(PT, w0 + x, 5, clock64());   // its block has landed
+#endif
         const Wave X(sring + tab[kTab * x].z);
         double* rem = reinterpret_cast<double*>(pkts(x) + 16 * X.NP);
         for (int j0 = 0; j0 < X.NP && !hung; j0 += 32) {
@@ -241,6 +252,9 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
         if (hung) break;
         __syncwarp();
       }
+#ifdef JV_REGION_TRACE
+      if (lane == 0) jv::trace_word(PT, w0 + x, 6, clock64());   // all values in
+#endif
       // release: the values written above are visible to whoever acquires
       if (lane == 0)
         asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(x + P) : "memory");
@@ -399,11 +413,17 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
   auto step = [&](int w, const Ops& cur, Ops& nxt, const Tab& tn, Tab& tnn) {
     // the prober has released this wave's remote dependencies (a wave
     // without any passes straight through)
+#ifdef JV_REGION_TRACE
+    if (tracing) jv::trace_clock(T, w0 + w, 1);   // wave start
+#endif
     if (cur.np > 0) {
       const int* const pr = probed + (w % kProbers);
       while (ld_acquire_shared(pr) <= w) {
       }
     }
+#ifdef JV_REGION_TRACE
+    if (tracing) jv::trace_clock(T, w0 + w, 2);   // released by the prober
+#endif
     double dv[kR];
     dv[0] = lds64(cur.r0.x);
     dv[1] = lds64(cur.r0.y);
@@ -470,9 +490,10 @@ __global__ void __launch_bounds__(NC + kExtra, 1) region_kernel(RArgs A) {
 #if !(JV_RDIAG & 4)
     if (pub) jv::mbox_put(mbox, row, res, epoch);
 #endif
-#if !(JV_RDIAG & 8)
-    asm volatile("bar.sync 1, %0;" ::"n"(kCompute + 32) : "memory");
+#ifdef JV_REGION_TRACE
+    if (tracing) jv::trace_clock(T, w0 + w, 4);   // computed, at the barrier
 #endif
+    asm volatile("bar.sync 1, %0;" ::"n"(kCompute + 32) : "memory");
 #ifdef JV_REGION_TRACE
     if (tracing) {
       if (flags & 16) jv::trace_clock(T, w0 + w, 7);   // 16: clock only (no globaltimer read)
@@ -602,7 +623,7 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const
   // barrier, no idle warps
   const int nc = max_rows > 0 && max_rows <= 128 ? 128
                  : max_rows > 0 && max_rows <= 256 ? 256 : jvr::kCompute;
-  const int block = nc + jvr::kExtra;
+  const int block = nc + jvr::extra_for(nc);
   const void* fn =
       nc == 128 ? (kind == 0 ? (const void*)jvr::region_kernel<0, 128>
                              : kind == 1 ? (const void*)jvr::region_kernel<1, 128>

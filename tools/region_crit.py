@@ -65,7 +65,7 @@ else:
 wl = np.array([lev[words[int(table[w, 0]) * 4 + 4 + 5]] for w in range(nw)])   # first record's row
 L = wl.max() + 1
 if os.environ.get("JV_CRIT_DUMP"):
-    np.savez_compressed(os.environ["JV_CRIT_DUMP"], g=tr[:, 0:8], c=c, wl=wl, rw=rw,
+    np.savez_compressed(os.environ["JV_CRIT_DUMP"], g=tr[:, 0:8], c=c,  wl=wl, rw=rw,
                         cnt=np.array([words[int(table[w, 0]) * 4] for w in range(nw)]),
                         npk=table[:, 7] >> 16)
 crit = np.array([np.argmax(np.where(wl == l, end, -1)) for l in range(L)])
