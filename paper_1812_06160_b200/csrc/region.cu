@@ -43,7 +43,7 @@ namespace jvr {
 
 constexpr int kThreads = 512;   // rows per wave (compute threads)
 constexpr int kNB = 16;   // static-block mbarriers in the ring (S + 1 <= kNB)
-constexpr int kTab = 3;   // int4 entries per wave in the shared-memory table
+constexpr int kTab = 1;   // int4 entries per wave in the shared-memory table
 constexpr int kL2 = 12;   // waves of L2 bulk prefetch ahead of the gathers (24 measured equal)
 
 struct RArgs {
@@ -154,17 +154,17 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
   int* done = reinterpret_cast<int*>(rsm + 8 * kNB);          // waves finished
   int* issued = done + 2;   // waves whose blocks the producer has issued
   int* probed = done + 8;   // [kProbers] per prober warp: its waves below this are released
-  int4* tab = reinterpret_cast<int4*>(rsm + 256);             // kTab per wave: the two table
-                                                              // entries and the block header
+  // per wave {static ring offset, dynamic ring offset, value bytes | vector
+  // bytes << 18, rows | K << 10 | remote packets << 16}
+  int4* tab = reinterpret_cast<int4*>(rsm + 256);
   unsigned char* sring = rsm + 256 + 16 * kTab * A.max_waves + 8 * A.SC;
   unsigned char* dring = sring + A.CS;
   const int w0 = A.reg_wave[blockIdx.x];
   const int nw = A.reg_wave[blockIdx.x + 1] - w0;
   for (int i = tid; i < nw; i += blockDim.x) {
-    const int4 t = A.table[2 * (w0 + i)];
-    tab[kTab * i] = t;
-    tab[kTab * i + 1] = A.table[2 * (w0 + i) + 1];
-    tab[kTab * i + 2] = A.words[t.x];   // {cnt, slot0, K, NP}: read before the block lands
+    const int4 t = A.table[2 * (w0 + i)], v = A.table[2 * (w0 + i) + 1];
+    const int4 hd = A.words[t.x];   // {cnt, slot0, K, NP}: read before the block lands
+    tab[i] = make_int4(t.z, t.w, v.y | ((v.w & 0xffff) << 18), hd.x | (hd.z << 10) | (hd.w << 16));
   }
   if (tid == 0) {
     for (int b = 0; b < kNB; ++b) bar_init(&bar[b], 1);
@@ -193,10 +193,10 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
     constexpr int P = kProbers;
     int* const myprobed = probed + pw;
     auto pkts = [&](int x) -> unsigned char* {
-      const int4 v = tab[kTab * x + 1];
-      return dring + tab[kTab * x].w + v.y + (v.w & 0xffff);
+      const int4 e = tab[x];
+      return dring + e.y + (e.z & 0x3ffff) + (e.z >> 18);
     };
-    auto np = [&](int x) { return tab[kTab * x + 1].w >> 16; };
+    auto np = [&](int x) { return (int)((unsigned)tab[x].w >> 16); };
     if (flags & 8) {   // diagnostic: no remote waits at all (wrong results)
       if (lane == 0)
         asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sa(myprobed)), "r"(nw + P) : "memory");
@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
 #ifdef JV_REGION_TRACE
         if (lane == 0) jv::trace_word(PT, w0 + x, 5, clock64());   // its block has landed
 #endif
-        const Wave X(sring + tab[kTab * x].z);
-        double* rem = reinterpret_cast<double*>(pkts(x) + 16 * X.NP);
+        const Wave X(sring + tab[x].x);
+        double* rem = reinterpret_cast<double*>(pkts(x));   // the wave's remote values
         for (int j0 = 0; j0 < X.NP && !hung; j0 += 32) {
           const int j = j0 + lane;
           bool need = j < X.NP;
@@ -292,21 +292,37 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
   if (tid >= kCompute) {
     // ------------------------------------------------------------ producer
     if (tid != kCompute) return;
-    auto prefetch = [&](int x) {
-      const int4 t2 = tab[kTab * x], v2 = tab[kTab * x + 1];
+    // (the full table entries come from global memory, one wave ahead in
+    // registers; shared memory keeps only what the other warps read)
+    const int4* gt = A.table + 2 * (int64_t)w0;
+    auto prefetch = [&](const int4& t2, const int4& v2) {
       l2_prefetch_bulk(A.words + t2.x, (uint32_t)t2.y);
       if (v2.y > 0) l2_prefetch_bulk(A.pack + 2 * (int64_t)v2.x, (uint32_t)v2.y);
       if (v2.w & 0xffff) l2_prefetch_bulk(A.vpack + 2 * (int64_t)v2.z, (uint32_t)(v2.w & 0xffff));
     };
     // (diagnostics: flags bits 8..15 override the L2 prefetch distance, 255 = none)
     const int kl2 = ((flags >> 8) & 255) == 255 ? 0 : ((flags >> 8) & 255) ? (int)((flags >> 8) & 255) : kL2;
-    for (int x = 0; x < kl2 && x < nw; ++x) prefetch(x);
+    for (int x = 0; x < kl2 && x < nw; ++x) prefetch(gt[2 * x], gt[2 * x + 1]);
+    int4 tn = gt[0], vn = gt[1];
+    int4 ptn = make_int4(0, 0, 0, 0), pvn = ptn;
+    if (kl2 && kl2 < nw) {
+      ptn = gt[2 * kl2];
+      pvn = gt[2 * kl2 + 1];
+    }
     for (int x = 0; x < nw; ++x) {
-      if (kl2 && x + kl2 < nw) prefetch(x + kl2);
+      const int4 t = tn, v = vn, pt = ptn, pv = pvn;
+      if (x + 1 < nw) {
+        tn = gt[2 * (x + 1)];
+        vn = gt[2 * (x + 1) + 1];
+      }
+      if (kl2 && x + 1 + kl2 < nw) {
+        ptn = gt[2 * (x + 1 + kl2)];
+        pvn = gt[2 * (x + 1 + kl2) + 1];
+      }
+      if (kl2 && x + kl2 < nw) prefetch(pt, pv);
       // ring blocks of wave x may overlap those of wave x - D - 1
       while (ld_volatile_shared(done) < x - D) __nanosleep(20);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int4 t = tab[kTab * x], v = tab[kTab * x + 1];
       uint64_t* b = &bar[x % kNB];
       const bool skip = flags & 4;   // diagnostic: no value copies (wrong results)
       const int cb = v.w & 0xffff;
@@ -356,15 +372,13 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
     int so, dof, vbytes, cnt, K, np;
   };
   auto load_tab = [&](int w, Tab& t) {
-    const int4 a0 = lds128(tab_off + 16 * kTab * w);
-    const int4 a1 = lds128(tab_off + 16 * kTab * w + 16);
-    const int4 hd = lds128(tab_off + 16 * kTab * w + 32);
-    t.so = a0.z;
-    t.dof = a0.w;
-    t.vbytes = a1.y;
-    t.cnt = hd.x;
-    t.K = hd.z;
-    t.np = hd.w;
+    const int4 e = lds128(tab_off + 16 * w);
+    t.so = e.x;
+    t.dof = e.y;
+    t.vbytes = e.z & 0x3ffff;
+    t.cnt = e.w & 1023;
+    t.K = (e.w >> 10) & 63;
+    t.np = (int)((unsigned)e.w >> 16);
   };
   // operands of a wave whose blocks have landed (the producer warp saw to
   // it before the last barrier): loads only, every address from registers

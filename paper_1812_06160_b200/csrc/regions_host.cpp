@@ -31,8 +31,8 @@
 //    ref with one load and no case distinction.  `me` is the offset of the
 //    row's own ring slot.  Dependencies beyond the fourth are in xref.
 //    The factor's u(c_k, r) come with the packed values.  The wave's dynamic
-//    block holds vals[NV][cnt] (matrix values), the per-call vector, NP
-//    16-byte mailbox packets and NP decoded doubles.  Static blocks are
+//    block holds vals[NV][cnt] (matrix values), the per-call vector and the
+//    NP remote values (doubles the prober warps read from the mailboxes).  Static blocks are
 //    bulk-copied (TMA) S waves ahead into a shared-memory ring, dynamic
 //    blocks D waves ahead; ring offsets are placed here by simulating both
 //    FIFO rings, and the remote refs are patched once the rings are placed.
@@ -40,6 +40,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -363,7 +365,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   };
   // shared-memory byte offsets the refs point to (region.cu's layout)
   const int32_t kOneOff = 144;                             // the constant 1.0
-  const int32_t slot_base = 256 + 48 * R->max_waves;       // value ring
+  const int32_t slot_base = 256 + 16 * R->max_waves;       // value ring
   auto emit = [&](int32_t SC) {
     std::fill(pub.begin(), pub.end(), 0);
     for (int32_t r = 0; r < n; ++r)
@@ -463,9 +465,9 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
         vidx.resize(c0 + cb / 8, -1);
         for (int32_t i = 0; i < cnt; ++i) vidx[c0 + i] = slot_row[s0 + i];
       }
-      // then the wave's 16-byte mailbox packets (filled by the prober warp)
+      // then the wave's remote values (8 bytes each, written by the prober warps)
       sbytes[w] = (int32_t)(4 * (W.size() - base));
-      dbytes[w] = vb + cb + 16 * (int32_t)pslot.size() + ((8 * (int32_t)pslot.size() + 15) & ~15);
+      dbytes[w] = vb + cb + ((8 * (int32_t)pslot.size() + 15) & ~15);
       npk[w] = (int32_t)pslot.size();
       ssz[g].push_back(sbytes[w]);
       dsz[g].push_back(dbytes[w]);
@@ -476,7 +478,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
   // in-region dependencies through the mailbox, where the D-wave prefetch
   // finds them long published)
   auto fit = [&](int64_t SC, int32_t& D_, int32_t& cs_, int32_t& cd_) {
-    const int64_t fixed = 512 + 48 * (int64_t)R->max_waves + 8 * SC;
+    const int64_t fixed = 512 + 16 * (int64_t)R->max_waves + 8 * SC;
     const int64_t ring = (smem_budget - fixed) & ~(int64_t)15;
     if (ring < 1024) return false;
     for (int D = 8; D >= 2; --D) {   // (the kernel's producer needs two waves of slack)
@@ -499,6 +501,14 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
     if (fit(SC, D, cs, cd) && D > bestD) {
       bestD = D;
       bestSC = SC;
+    }
+    if (std::getenv("JV_RS_DEBUG")) {
+      int32_t ms = 0, md = 0;
+      for (auto& v : ssz) for (int32_t x : v) ms = std::max(ms, x);
+      for (auto& v : dsz) for (int32_t x : v) md = std::max(md, x);
+      std::fprintf(stderr, "rstream kind %d threads %d SC %lld: max static block %d, max dynamic block %d, "
+                   "max_waves %d, budget %lld -> D %d\n", kind, threads, (long long)SC, ms, md,
+                   R->max_waves, (long long)smem_budget, D);
     }
     if (bestD >= 6) break;
   }
@@ -530,8 +540,7 @@ extern "C" int64_t jv_rstream_build(int32_t kind, int32_t n, const int32_t* rs, 
       R->table[8 * w + 7] = cbytes[w] | (npk[w] << 16);   // | remote packets of the wave
       // remote refs -> offsets of the wave's decoded values (behind its
       // packed values, vector and packets in the dynamic ring)
-      const int32_t rem = slot_base + 8 * R->SC + R->CS + dof[k] + vbytes[w] + cbytes[w] +
-                          16 * npk[w];
+      const int32_t rem = slot_base + 8 * R->SC + R->CS + dof[k] + vbytes[w] + cbytes[w];
       int32_t* blk = &W[(size_t)goff[w] * 4];
       const int32_t cnt = blk[0], K = blk[2];
       for (int32_t i = 0; i < cnt; ++i)

@@ -128,9 +128,9 @@ def records(ws: WaveStream, w):
     xref = blk[4 + 8 * cnt:4 + (8 + kx) * cnt].reshape(kx, cnt)
     off = 4 + (8 + kx) * cnt
     pslot = blk[off:off + NP]
-    slot_base = 256 + 48 * ws.max_waves
+    slot_base = 256 + 16 * ws.max_waves
     rem_base = slot_base + 8 * ws.slot_ring + ws.CS + int(ws.table[w, 3]) + int(ws.table[w, 5]) + \
-        (int(ws.table[w, 7]) & 0xFFFF) + 16 * NP
+        (int(ws.table[w, 7]) & 0xFFFF)
 
     def back(off):
         off = int(off)

@@ -196,9 +196,9 @@ def _ring_ok(ws):
                 if kind == "s":
                     size = int(ws.table[w, 1])
                 else:
-                    npk = int(ws.table[w, 7]) >> 16   # packets + their decoded doubles
+                    npk = int(ws.table[w, 7]) >> 16   # remote values, 8 bytes each
                     size = int(ws.table[w, 5]) + (int(ws.table[w, 7]) & 0xFFFF) + \
-                        16 * npk + ((8 * npk + 15) & ~15)
+                        ((8 * npk + 15) & ~15)
                 off = int(ws.table[w, col_off])
                 assert off % 16 == 0 and off + size <= cap
                 for (o2, s2) in blocks[-win:]:
