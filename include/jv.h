@@ -346,6 +346,9 @@ int jv_region_threads(void);
  * the value bulk copies, 8 the remote-dependency waits; 0 in production */
 int jv_set_region_flags(unsigned flags);
 int64_t jv_region_smem_fixed(int32_t max_region, int32_t max_waves);
+/* max_rows: low 16 bits = most rows in a wave (picks 128 / 256 / 512 compute
+ * threads), high bits = most dependencies of a row in any wave (0 = unknown;
+ * <= 3 picks the three-dependency instances) */
 int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const void* words,
                   const int32_t* table,
                   const int32_t* reg_wave, int32_t max_region, int32_t max_waves, int32_t S,

@@ -35,6 +35,9 @@
 // waits on rows of lower levels; all CTAs are co-resident (cooperative
 // launch), so the lowest pending level always progresses.
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
 #include "../../include/jv.h"
@@ -143,7 +146,7 @@ JV_INLINE int ld_volatile_shared(const int* p) {
 // all addressed from the wave table alone, up to D waves ahead of the
 // compute warps (whose progress it reads from a shared counter before
 // reusing ring space), with L2 bulk prefetches kL2 waves further ahead.
-template <int KIND, int NC = kCompute>
+template <int KIND, int NC, int KR, bool TAU>
 __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) {
   constexpr int kCompute = NC;
   constexpr int kProbers = probers_for(NC);   // compute threads: waves of at most NC rows
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
   }
   __syncthreads();
   const int D = A.D;
-  const bool tau = KIND == 0 && A.tau > 0.0;
+  constexpr bool tau = KIND == 0 && TAU;   // (the launch picks the instance from A.tau)
   const unsigned flags = jv::g_region_flags;
 
   if (tid >= kCompute + 64) {
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
   // off, and the only branches are the remote-wave wait, the rare slow
   // division and the rare zero pivot.  Critical path per wave:
   //   barrier -> dependency loads -> arithmetic chain -> slot store -> barrier.
-  constexpr int kR = 4;   // dependencies held in registers
+  constexpr int kR = KR;   // dependencies held in registers (every row's, for the factor)
   const uint32_t sb = sa(rsm);
   auto lds64 = [&](uint32_t off) -> double {
     double v;
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
         s.u[k] = lds64(vp + (K + min(k + 1, K)) * c8);
       }
       s.dg = lds64(vp + K * c8);
-      s.rhs = lds64(tau ? vec : vp);   // the row's norm when tau > 0 (no vector block otherwise)
+      s.rhs = tau ? lds64(vec) : 0.0;   // the row's norm (no vector block without tau)
     } else {
       const int o = KIND == 1 ? 0 : 1;
 #pragma unroll
@@ -424,13 +427,16 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
   const jv::Trace T = jv::trace_begin();
   const bool tracing = T.p != nullptr && tid == 0;
 #endif
+  int rel = 0;   // the release counter of the coming wave's prober, read a wave early
   auto step = [&](int w, const Ops& cur, Ops& nxt, const Tab& tn, Tab& tnn) {
     // the prober has released this wave's remote dependencies (a wave
     // without any passes straight through)
 #ifdef JV_REGION_TRACE
     if (tracing) jv::trace_clock(T, w0 + w, 1);   // wave start
 #endif
-    if (cur.np > 0) {
+    // (its counter was read during the wave before: no load on the
+    // critical path when the prober is ahead)
+    if (cur.np > 0 && rel <= w) {
       const int* const pr = probed + (w % kProbers);
       while (ld_acquire_shared(pr) <= w) {
       }
@@ -442,12 +448,13 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
     dv[0] = lds64(cur.r0.x);
     dv[1] = lds64(cur.r0.y);
     dv[2] = lds64(cur.r0.z);
-    dv[3] = lds64(cur.r0.w);
+    if (kR > 3) dv[kR - 1] = lds64(cur.r0.w);
     // the next wave's operands, in flight during this wave's arithmetic
     // (after the last wave: that wave again, its blocks are still there),
     // and the table entries of the wave after it
     fetch(tn, nxt);
     load_tab(min(w + 2, nw - 1), tnn);
+    rel = ld_acquire_shared(probed + ((w + 1) % kProbers));
     const int cnt = cur.cnt, K = cur.K;
     const bool active = tid < cnt;
     const int meta = cur.r1.z, nd = meta & 63, row = cur.r1.y, p0 = cur.r1.x;
@@ -461,13 +468,13 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
 #endif
       // pivots beyond the row's own: a = +0.0 (K > k >= nd) or a copy of an
       // earlier operand (k >= K), never used: umask and the stores are per nd
-      double l[4];
-      jv::ddiv_batch<4>(cur.a, dv, l, nd);   // (four interleaved chains cost the latency of one)
-      const double thresh = jv::dmul(tauv, cur.rhs);
+      double l[kR];
+      jv::ddiv_batch<kR>(cur.a, dv, l, nd);   // (interleaved chains: the latency of one)
+      const double thresh = tau ? jv::dmul(tauv, cur.rhs) : 0.0;
       double d = cur.dg;
       const int umask = (meta >> 7) & 15;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kR; ++k) {
         const bool drop = tau && fabs(l[k]) < thresh;
         const double dn = jv::dsub(d, jv::dmul(l[k], cur.u[k]));
         d = (!drop && (umask & (1 << k))) ? dn : d;
@@ -476,7 +483,7 @@ __global__ void __launch_bounds__(NC + extra_for(NC), 1) region_kernel(RArgs A) 
       res = d;
 #if !(JV_RDIAG & 4)
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < kR; ++k)
         if (active && k < nd) __stcg(gval + p0 + k, l[k]);
       if (active) __stcg(gval + p0 + nd, d);
       if (active && d == 0.0) atomicMin(A.err, row);
@@ -635,24 +642,48 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const
   const size_t smem = (size_t)jv_region_smem_fixed(slot_ring, max_waves) + CS + CD;
   // waves of at most 256 (128) rows run on 8 (4) compute warps: a cheaper
   // barrier, no idle warps
-  const int nc = max_rows > 0 && max_rows <= 128 ? 128
-                 : max_rows > 0 && max_rows <= 256 ? 256 : jvr::kCompute;
+  const int mr = max_rows & 0xffff;
+  const int nc = mr > 0 && mr <= 128 ? 128 : mr > 0 && mr <= 256 ? 256 : jvr::kCompute;
   const int block = nc + jvr::extra_for(nc);
-  const void* fn =
-      nc == 128 ? (kind == 0 ? (const void*)jvr::region_kernel<0, 128>
-                             : kind == 1 ? (const void*)jvr::region_kernel<1, 128>
-                                         : (const void*)jvr::region_kernel<2, 128>)
-      : nc == 256 ? (kind == 0 ? (const void*)jvr::region_kernel<0, 256>
-                               : kind == 1 ? (const void*)jvr::region_kernel<1, 256>
-                                           : (const void*)jvr::region_kernel<2, 256>)
-                  : (kind == 0 ? (const void*)jvr::region_kernel<0>
-                               : kind == 1 ? (const void*)jvr::region_kernel<1>
-                                           : (const void*)jvr::region_kernel<2>);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run attr");
+  const int kmax = max_rows >> 16;   // most dependencies of a row (0: unknown)
+  if (kind == 0 && kmax > 4) {
+    jvh::set_error("jv_region_run: factor rows with %d pivots", kmax);
+    return JV_EINVAL;
+  }
+  const bool k3 = kmax > 0 && kmax <= 3;
+  const bool tt = kind == 0 && tau > 0.0;
+  const void* fn = nullptr;
+#define JV_RK(K, N)                                                                           \
+  (k3 ? (tt ? (const void*)jvr::region_kernel<K, N, 3, (K == 0)>                              \
+            : (const void*)jvr::region_kernel<K, N, 3, false>)                                \
+      : (tt ? (const void*)jvr::region_kernel<K, N, 4, (K == 0)>                              \
+            : (const void*)jvr::region_kernel<K, N, 4, false>))
+#define JV_RKN(K) (nc == 128 ? JV_RK(K, 128) : nc == 256 ? JV_RK(K, 256) : JV_RK(K, 512))
+  fn = kind == 0 ? JV_RKN(0) : kind == 1 ? JV_RKN(1) : JV_RKN(2);
+#undef JV_RKN
+#undef JV_RK
+  // attributes and residency are checked once per (instance, shared memory
+  // size); the size attribute of an instance only ever grows
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> resident;
+  static std::map<const void*, size_t> attr;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem);
-  if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run occupancy");
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = resident.find({fn, smem});
+    if (it != resident.end()) per_sm = it->second;
+    if (per_sm == 0) {
+      cudaError_t e = cudaSuccess;
+      if (attr[fn] < smem) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run attr");
+        attr[fn] = smem;
+      }
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem);
+      if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run occupancy");
+      resident[{fn, smem}] = per_sm;
+    }
+  }
   if (per_sm * jvh::sm_count() < nreg) {
     jvh::set_error("jv_region_run: %d regions but only %d resident CTAs", nreg,
                    per_sm * jvh::sm_count());
@@ -662,7 +693,7 @@ extern "C" int jv_region_run(int32_t kind, int32_t nreg, int32_t max_rows, const
                reg_wave, slot_ring, max_waves, S, D, CS, CD, val, pack, vpack, out, norms, tau, mbox,
                epoch, err_row};
   void* args[] = {&A};
-  e = cudaLaunchCooperativeKernel(fn, dim3(nreg), dim3(block), args, smem,
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(nreg), dim3(block), args, smem,
                                   (cudaStream_t)stream);
   if (e != cudaSuccess) return jvh::cuda_status(e, "jv_region_run");
   return JV_OK;

@@ -739,8 +739,9 @@ class DevIlu:
     # times all of them against the ticket kernel (measured: config 2's
     # factor prefers 144 pencils, its solves 64 pencils; config 3 100 boxes,
     # config 4 144 boxes)
-    region_candidates = {"factor": [(2, 0), (3, 0)],
-                         "fwd": [(3, 0), (2, 64), (3, 100)], "bwd": [(3, 0), (2, 64), (3, 100)]}
+    region_candidates = {"factor": [(2, 0), (3, 0), (2, 64)],
+                         "fwd": [(3, 0), (2, 64), (3, 100), (2, 0)],
+                         "bwd": [(3, 0), (2, 64), (3, 100), (2, 0)]}
 
     def regions(self, dims=0, rmax=0):
         """(nreg, region_of) or None."""
@@ -801,7 +802,8 @@ class DevIlu:
                     vidx=up(ws.vidx) if mv else None, mv=mv,
                     vpack=t.empty(max(mv, 2), dtype=t.float64, device="cuda"),
                     slot_ring=ws.slot_ring, max_waves=ws.max_waves, S=ws.S, D=ws.D, CS=ws.CS,
-                    CD=ws.CD, waves=ws.waves, remote_deps=ws.remote_deps, max_rows=ws.max_rows)
+                    CD=ws.CD, waves=ws.waves, remote_deps=ws.remote_deps, max_rows=ws.max_rows,
+                    kmax=int(ws.words[ws.table[:, 0].astype(np.int64) * 4 + 2].max()))
 
     def values_changed(self):
         """Invalidate the wave-ordered value copies (call after writing val)."""
@@ -854,7 +856,7 @@ class DevIlu:
                       ptr(reset), stream())
         if before_kernel is not None:
             before_kernel()
-        _lib.call("jv_region_run", kind, rp["nreg"], rp["max_rows"], ptr(rp["words"]),
+        _lib.call("jv_region_run", kind, rp["nreg"], rp["max_rows"] | (rp["kmax"] << 16), ptr(rp["words"]),
                   ptr(rp["table"]),
                   ptr(rp["reg_wave"]), rp["slot_ring"], rp["max_waves"], rp["S"],
                   min(rp["D"], _REGION_D_CAP),
