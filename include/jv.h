@@ -88,12 +88,17 @@ int jv_test_ddiv(int32_t n, const double* a, const double* b, double* out, void*
 /* ---- spmv: y = A x ---------------------------------------------------
  * replaces _kernels.py:28-34 spmv_kernel (called by csr.py:251-260 spmv).
  * Row sums are accumulated in ascending column order without FMA, so the
- * result is bitwise equal to the reference for every row of up to
- * jv_spmv_tile() entries; longer rows use a tree sum (within 1e-12).
+ * result is bitwise equal to the reference for rows of any length.
+ * Two kernels, same bits: a CTA-per-tile stream kernel (small matrices)
+ * and a persistent kernel whose col/val tiles arrive by bulk copies (TMA)
+ * in a shared-memory ring (from 2^20 nonzeros; col and val 16-byte
+ * aligned, else its tiles are loaded directly).  jv_set_spmv_impl: -1 by
+ * size (default), 0 stream, 1 persistent.
  * tile_rows (nullable) is the jv_spmv_plan output, int32[2*(ntiles+1)]
  * (first row of each tile boundary and that row's first nonzero) with
  * ntiles = max(1, ceil(nnz / jv_spmv_tile())).                           */
 int jv_spmv_tile(void);
+int jv_set_spmv_impl(int impl);
 int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, int32_t* tile_rows,
                  void* stream);
 int jv_spmv(int32_t n, int32_t nnz, const int32_t* row_start, const int32_t* col,

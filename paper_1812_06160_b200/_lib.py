@@ -41,6 +41,7 @@ _SIGS = {
     "jv_set_trace": [_P, ctypes.c_longlong],
     "jv_test_ddiv": [c_int32, _P, _P, _P, _P],
     "jv_spmv_tile": [],
+    "jv_set_spmv_impl": [c_int],
     "jv_spmv_plan": [c_int32, c_int32, _P, _P, _P],
     "jv_spmv": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P],
     "jv_spmv_rows": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -22,7 +22,7 @@ namespace {
 #define JV_SPMV_THREADS 128
 #endif
 #ifndef JV_SPMV_TILE
-#define JV_SPMV_TILE 640
+#define JV_SPMV_TILE 512
 #endif
 constexpr int kSpmvThreads = JV_SPMV_THREADS;
 constexpr int kTile = JV_SPMV_TILE;  // nonzeros per CTA tile
@@ -127,9 +127,249 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_stream_kernel(
   if (threadIdx.x == 0) y[row_map ? row_map[rlast] : rlast] = acc;
 }
 
+
+// ---------------------------------------------------------------------
+// Persistent bulk-copy variant (large matrices; needs the jv_spmv_plan map).
+// The nonzero stream is cut into tiles of T = M*kTile entries; CTA b walks
+// the tiles [b*tpc, (b+1)*tpc):
+//   * one thread bulk-copies (TMA, cp.async.bulk + mbarrier complete_tx) the
+//     col and val tiles S tiles ahead into a shared-memory ring — S*12T
+//     bytes per CTA in flight at no register or LSU cost;
+//   * the x gathers of tile j+1 are issued (col read from shared memory)
+//     before the row sums of tile j, so their L2/DRAM latency runs beside
+//     the sums; products go to a double-buffered shared array;
+//   * the rows that START in tile k are [F_k, F_{k+1}) with F from the plan
+//     (first row whose first nonzero is >= k*T), so every tile's row range —
+//     and the row bounds its threads need — is known a tile ahead, without
+//     searching; each row that ENDS in the tile is summed serially by one
+//     thread in the reference order; the one row that runs on into the next
+//     tile hands its partial sum over in shared memory (the sum stays one
+//     left-to-right chain: bitwise the reference for rows of any length).
+// A CTA whose first tile begins inside a row first folds that row's earlier
+// entries (whole CTA forms the products chunk by chunk, one thread adds them
+// in order).  Global traffic is the 12 nnz + 20 n algorithmic bytes.
+template <int T, int S, int NT>
+struct BulkSmem {
+  double val[S][T];
+  double prod[2][T];
+  int32_t col[S][T];
+  uint64_t bar[S];
+  double carry[2];
+};
+
+JV_INLINE uint32_t sp_sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+JV_INLINE void sp_bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra SW_%=;\n}" ::"r"(sp_sa(b)), "r"(parity) : "memory");
+}
+JV_INLINE void sp_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;"
+      ::"r"(sp_sa(dst)), "l"(src), "r"(bytes), "r"(sp_sa(b)), "l"(pol) : "memory");
+}
+
+template <int T, int S, int NT>
+__global__ void __launch_bounds__(NT) spmv_bulk_kernel(
+    int n, int nnz, int ntiles, int tpc, int staged, const int32_t* __restrict__ rs,
+    const int32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, double* __restrict__ y, const int2* __restrict__ plan,
+    const int32_t* __restrict__ row_map) {
+  static_assert(T % kTile == 0 && T % NT == 0, "plan entries are per kTile nonzeros");
+  constexpr int kM = T / kTile;
+  constexpr int kU = T / NT;
+  extern __shared__ __align__(128) unsigned char sp_raw[];
+  BulkSmem<T, S, NT>& sm = *reinterpret_cast<BulkSmem<T, S, NT>*>(sp_raw);
+  const int tid = threadIdx.x;
+  const int kb = blockIdx.x * tpc;
+  const int nt = min(kb + tpc, ntiles) - kb;   // > 0 by the grid's construction
+  // (first row starting at or behind tile k's first nonzero, that row's start)
+  auto first_row = [&](int k) { return k >= ntiles ? make_int2(n, nnz) : __ldg(plan + kM * k); };
+  uint64_t pol = 0;
+  if (tid == 0) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (int s = 0; s < S; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sp_sa(&sm.bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto is_full = [&](int j) { return staged && (long long)(kb + j + 1) * T <= nnz; };
+  auto issue = [&](int j) {   // thread 0: fetch the CTA's j-th tile into its ring stage
+    if (!is_full(j)) return;
+    const long long p = (long long)(kb + j) * T;
+    uint64_t* bar = &sm.bar[j % S];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(sp_sa(bar)), "r"((uint32_t)(T * 12)) : "memory");
+    sp_bulk(sm.val[j % S], val + p, T * 8, bar, pol);
+    sp_bulk(sm.col[j % S], col + p, T * 4, bar, pol);
+  };
+  if (tid == 0)
+    for (int j = 0; j < S && j < nt; ++j) issue(j);
+
+  int2 f0 = first_row(kb), f1 = first_row(kb + 1);
+  // a row running into the CTA's first tile: fold its earlier entries
+  {
+    const int ts0 = kb * T;
+    double acc = 0.0;
+    if (f0.y > ts0) {
+      const int a = __ldg(rs + f0.x - 1);
+      for (int c0 = a; c0 < ts0; c0 += T) {
+        const int c1 = min(c0 + T, ts0);
+        __syncthreads();
+        for (int q = c0 + tid; q < c1; q += NT)
+          sm.prod[1][q - c0] = jv::dmul(__ldg(val + q), __ldg(x + __ldg(col + q)));
+        __syncthreads();
+        if (tid == 0)
+          for (int q = 0; q < c1 - c0; ++q) acc = jv::dadd(acc, sm.prod[1][q]);
+      }
+    }
+    if (tid == 0) sm.carry[0] = acc;   // read behind the first tile's barrier
+  }
+
+  // gathers of one tile: x values (and, for an unstaged tile, the matrix values) in registers
+  double xv[kU], vv[kU];
+  auto gather = [&](int j) {
+    const int ts = (kb + j) * T;
+    if (is_full(j)) {
+      sp_bar_wait(&sm.bar[j % S], (uint32_t)((j / S) & 1));
+      const int32_t* sc = sm.col[j % S];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) xv[u] = __ldg(x + sc[tid + u * NT]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int q = ts + tid + u * NT;
+        const bool in = q < nnz;
+        vv[u] = in ? __ldcs(val + q) : 0.0;
+        xv[u] = in ? __ldg(x + __ldcs(col + q)) : 0.0;
+      }
+    }
+  };
+  int rc = f0.x - (f0.y > kb * T ? 1 : 0);   // first row ending in the current tile
+  int r0 = rc + tid, ra = 0, rb = 0;          // this thread's first row of the tile, its bounds
+  if (r0 < f1.x) { ra = __ldg(rs + r0); rb = __ldg(rs + r0 + 1); }
+  gather(0);
+  for (int j = 0; j < nt; ++j) {
+    const int k = kb + j;
+    const int ts = k * T;
+    const int te = (int)min((long long)ts + T, (long long)nnz);
+    double* prod = sm.prod[j & 1];
+    if (is_full(j)) {
+      const double* sv = sm.val[j % S];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) prod[tid + u * NT] = jv::dmul(sv[tid + u * NT], xv[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) prod[tid + u * NT] = jv::dmul(vv[u], xv[u]);
+    }
+    __syncthreads();
+    // the tile's ring stage is free: refill it; then the next tile's gathers and row bounds
+    if (tid == 0 && j + S < nt) issue(j + S);
+    const int2 f2 = first_row(k + 2);
+    const int rl = f1.x - 1;                       // last row starting in this tile
+    const int rcn = f1.x - (f1.y > te ? 1 : 0);    // first row ending in the next tile
+    const int rn0 = rcn + tid;
+    int rna = 0, rnb = 0;
+    if (j + 1 < nt) {
+      gather(j + 1);
+      if (rn0 < f2.x) { rna = __ldg(rs + rn0); rnb = __ldg(rs + rn0 + 1); }
+    }
+    const double cin = sm.carry[j & 1];
+    for (int r = r0; r <= rl; r += NT) {
+      if (r != r0) { ra = __ldg(rs + r); rb = __ldg(rs + r + 1); }
+      double s = r == rc ? cin : 0.0;
+      const int qb = min(rb, te) - ts;
+      int q = max(ra, ts) - ts;
+      for (; q + 4 <= qb; q += 4) {   // four loads in flight, added in order
+        const double p0 = prod[q], p1 = prod[q + 1], p2 = prod[q + 2], p3 = prod[q + 3];
+        s = jv::dadd(jv::dadd(jv::dadd(jv::dadd(s, p0), p1), p2), p3);
+      }
+      for (; q < qb; ++q) s = jv::dadd(s, prod[q]);
+      if (rb <= te) {
+        __stcs(y + (row_map ? __ldg(row_map + r) : r), s);
+        if (r == rl) sm.carry[(j + 1) & 1] = 0.0;
+      } else {
+        sm.carry[(j + 1) & 1] = s;   // r == rl: the row runs on into the next tile
+      }
+    }
+    f1 = f2;
+    rc = rcn;
+    r0 = rn0;
+    ra = rna;
+    rb = rnb;
+  }
+}
+
+int g_spmv_impl = -1;   // -1 auto, 0 stream, 1 bulk
+
+template <int M, int S, int NT>
+void spmv_bulk_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const double* val,
+                      const double* x, double* y, const int32_t* tile_rows,
+                      const int32_t* row_map, cudaStream_t st) {
+  constexpr int T = M * kTile;
+  using Sm = BulkSmem<T, S, NT>;
+  static int resident = [] {
+    cudaFuncSetAttribute(spmv_bulk_kernel<T, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(Sm));
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_bulk_kernel<T, S, NT>, NT,
+                                                  sizeof(Sm));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return max(occ, 1) * sms;
+  }();
+  const int ntiles = (int)(((long long)nnz + T - 1) / T);
+  const int tpc = (ntiles + resident - 1) / resident;
+  const int grid = (ntiles + tpc - 1) / tpc;
+  const int staged =
+      ((reinterpret_cast<uintptr_t>(col) | reinterpret_cast<uintptr_t>(val)) & 15) == 0;
+  spmv_bulk_kernel<T, S, NT><<<grid, NT, sizeof(Sm), st>>>(
+      n, nnz, ntiles, tpc, staged, rs, col, val, x, y, reinterpret_cast<const int2*>(tile_rows),
+      row_map);
+}
+
+void spmv_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const double* val,
+                 const double* x, double* y, const int32_t* tile_rows, const int32_t* row_map,
+                 cudaStream_t st) {
+  static const int env = [] {
+    const char* e = getenv("JV_SPMV_IMPL");
+    return e ? atoi(e) : -1;
+  }();
+  static const int cfg = [] {
+    const char* e = getenv("JV_SPMV_CFG");   // tuning: ring depth / threads of the bulk kernel
+    return e ? atoi(e) : 0;
+  }();
+  const int impl = g_spmv_impl >= 0 ? g_spmv_impl : env;
+  const bool bulk = tile_rows != nullptr && nnz > 0 && (impl == 1 || (impl < 0 && nnz >= (1 << 20)));
+  if (!bulk) {
+    const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
+    spmv_stream_kernel<<<ntiles, kSpmvThreads, 0, st>>>(n, nnz, rs, col, val, x, y, tile_rows,
+                                                       row_map);
+    return;
+  }
+#define JV_SPMV_ARGS n, nnz, rs, col, val, x, y, tile_rows, row_map, st
+  switch (cfg) {
+    case 1: spmv_bulk_launch<2, 2, 256>(JV_SPMV_ARGS); break;
+    case 2: spmv_bulk_launch<1, 3, 128>(JV_SPMV_ARGS); break;
+    case 3: spmv_bulk_launch<1, 4, 128>(JV_SPMV_ARGS); break;
+    case 4: spmv_bulk_launch<1, 2, 256>(JV_SPMV_ARGS); break;
+    case 5: spmv_bulk_launch<1, 3, 256>(JV_SPMV_ARGS); break;
+    case 6: spmv_bulk_launch<2, 3, 256>(JV_SPMV_ARGS); break;
+    case 7: spmv_bulk_launch<2, 2, 512>(JV_SPMV_ARGS); break;
+    default: spmv_bulk_launch<1, 2, 128>(JV_SPMV_ARGS); break;
+  }
+#undef JV_SPMV_ARGS
+}
+
 }  // namespace
 
 extern "C" int jv_spmv_tile(void) { return kTile; }
+
+// -1: by size (bulk from 2^20 nonzeros), 0: CTA-per-tile stream kernel, 1: persistent bulk kernel
+extern "C" int jv_set_spmv_impl(int impl) { g_spmv_impl = impl; return JV_OK; }
 
 extern "C" int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, int32_t* tile_rows,
                             void* stream) {
@@ -146,10 +386,7 @@ extern "C" int jv_spmv(int32_t n, int32_t nnz, const int32_t* row_start, const i
                        void* stream) {
   if (n < 0 || nnz < 0) { jvh::set_error("jv_spmv: bad size"); return JV_EINVAL; }
   if (n == 0) return JV_OK;
-  const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
-  spmv_stream_kernel<<<ntiles, kSpmvThreads, 0, (cudaStream_t)stream>>>(n, nnz, row_start, col,
-                                                                        val, x, y, tile_rows,
-                                                                        nullptr);
+  spmv_launch(n, nnz, row_start, col, val, x, y, tile_rows, nullptr, (cudaStream_t)stream);
   JV_CHECK_LAUNCH("jv_spmv");
   return JV_OK;
 }
@@ -159,10 +396,7 @@ extern "C" int jv_spmv_rows(int32_t n, int32_t nnz, const int32_t* row_start, co
                             const int32_t* tile_rows, const int32_t* row_map, void* stream) {
   if (n < 0 || nnz < 0) { jvh::set_error("jv_spmv_rows: bad size"); return JV_EINVAL; }
   if (n == 0) return JV_OK;
-  const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
-  spmv_stream_kernel<<<ntiles, kSpmvThreads, 0, (cudaStream_t)stream>>>(n, nnz, row_start, col,
-                                                                        val, x, y, tile_rows,
-                                                                        row_map);
+  spmv_launch(n, nnz, row_start, col, val, x, y, tile_rows, row_map, (cudaStream_t)stream);
   JV_CHECK_LAUNCH("jv_spmv_rows");
   return JV_OK;
 }

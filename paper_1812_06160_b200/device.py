@@ -133,9 +133,14 @@ def pinned_host(a):
     return isinstance(a, np.ndarray) and a.dtype == np.float64 and _registered(a)
 
 
-def upload_f64(dst, src):
+VEC_CHUNK = 1 << 17   # doubles per staging chunk for vectors (1 MB)
+_PIN_RESULT_MIN = 1 << 17   # doubles: results at least this long come back in pinned memory
+
+
+def upload_f64(dst, src, chunk=None):
     """dst (device tensor) <- src (host float64 numpy array)."""
     t = torch()
+    chunk = chunk or _CHUNK
     if isinstance(src, np.ndarray) and src.dtype == np.float64 and _registered(src):
         _lib.call("jv_memcpy_async", ptr(dst), ctypes.c_void_p(src.ctypes.data), src.nbytes, 0,
                   stream())
@@ -147,12 +152,38 @@ def upload_f64(dst, src):
         return dst
     pin = _pinned(n)
     hsrc = t.from_numpy(src)
-    for a in range(0, n, _CHUNK):
-        b = min(n, a + _CHUNK)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
         pin[a:b].copy_(hsrc[a:b])
         dst[a:b].copy_(pin[a:b], non_blocking=True)
     _mark_busy()
     return dst
+
+
+def upload_vec(src, n):
+    """New device vector <- host vector of length n (the per-call right-hand
+    side of the drop-in solves): small staging chunks, so the host copy of
+    one chunk runs beside the DMA of the previous one."""
+    src = np.asarray(src, dtype=np.float64)
+    if src.shape != (n,):
+        raise ValueError(f"vector of shape {src.shape} for a system of {n} rows")
+    x = empty_f64(n)
+    upload_f64(x, src, chunk=VEC_CHUNK)
+    return x
+
+
+def download_vec(src, n):
+    """Fresh host vector <- src[:n] (device).  Long results are written by
+    one DMA straight into page-locked memory from torch's caching host
+    allocator (the block goes back to the cache when the caller drops the
+    array), so there is no staging copy and no first-touch page faulting."""
+    t = torch()
+    if n < _PIN_RESULT_MIN:
+        return host_f64(src, n)
+    out = t.empty(n, dtype=t.float64, pin_memory=True)
+    out.copy_(src[:n], non_blocking=True)
+    sync()
+    return out.numpy()
 
 
 def download_f64(dst, src, n=None):

@@ -56,18 +56,17 @@ def _check_schedule(factors: IluFactors, schedule, partition=None) -> None:
 
 
 def _device_sweep(factors: IluFactors, b: np.ndarray, which: str) -> np.ndarray:
-    b = np.array(b, dtype=np.float64, copy=True)
     if factors.n == 0:
-        return b
+        return np.array(b, dtype=np.float64, copy=True)
     d = factors.upload_values()
     if which == BACKWARD:
         bad = d.first_zero_diag()
         if bad >= 0:
             raise ZeroPivotError(bad)
-    x = dv.f64(b)
+    x = dv.upload_vec(b, factors.n)
     d.solve_async(0 if which == FORWARD else 1, x, x)
     dv.check_hang()
-    return dv.host_f64(x, factors.n)
+    return dv.download_vec(x, factors.n)
 
 
 def solve_serial(factors: IluFactors, b: np.ndarray, which: str) -> np.ndarray:
@@ -90,17 +89,16 @@ def solve_baseline_csrls(
     _check_which(which)
     if schedule.n != factors.n:
         raise ConfigurationError("level schedule does not match the factors")
-    b = np.array(b, dtype=np.float64, copy=True)
     if factors.n == 0:
-        return b
+        return np.array(b, dtype=np.float64, copy=True)
     d = factors.upload_values()
     if which == BACKWARD:
         bad = d.first_zero_diag()
         if bad >= 0:
             raise ZeroPivotError(bad)
-    x = dv.f64(b)
+    x = dv.upload_vec(b, factors.n)
     d.solve_csrls_async(0 if which == FORWARD else 1, x, x)
-    return dv.host_f64(x, factors.n)
+    return dv.download_vec(x, factors.n)
 
 
 def solve_ls(
@@ -184,15 +182,14 @@ def apply_preconditioner(
     the device, one upload and one download."""
     if setup is not None and setup.path not in ("serial", "csrls", "ls", "ls_lower"):
         raise ConfigurationError(f"unknown solve path {setup.path!r}")
-    z = np.array(r, dtype=np.float64, copy=True)
     if factors.n == 0:
-        return z
+        return np.array(r, dtype=np.float64, copy=True)
     d = factors.upload_values()
-    x = dv.f64(z)
+    x = dv.upload_vec(r, factors.n)
     d.solve_async(0, x, x)
     bad = d.first_zero_diag()
     if bad >= 0:
         raise ZeroPivotError(bad)
     d.solve_async(1, x, x)
     dv.check_hang()
-    return dv.host_f64(x, factors.n)
+    return dv.download_vec(x, factors.n)

@@ -27,42 +27,39 @@ plan.permuted.tile_rows()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 
 
-def med(fn, reps=10):
-    ts = []
+def span(fn, reps=20):
+    """Average time of fn() over `reps` back-to-back calls (one event pair:
+    single-launch event times are quantised to ~2 us)."""
+    fn()
+    torch.cuda.synchronize()
+    ev[0].record()
     for _ in range(reps):
-        t = fn()
-        ts.append(t)
-    return float(np.median(ts))
-
-
-def b2b():
-    dv.spmv_dev(plan.permuted, b, sy)
-    ev[0].record()
-    dv.spmv_dev(plan.permuted, b, sy)
+        fn()
     ev[1].record()
     torch.cuda.synchronize()
-    return ev[0].elapsed_time(ev[1]) * 1e3
+    return ev[0].elapsed_time(ev[1]) * 1e3 / reps
 
 
-def after_bwd():
+def med(fn, n=5):
+    return float(np.median([fn() for _ in range(n)]))
+
+
+def spmv():
+    dv.spmv_dev(plan.permuted, b, sy)
+
+
+def bwd():
     ilu.solve_async(1, y, x)
-    ev[0].record()
-    dv.spmv_dev(plan.permuted, b, sy)
-    ev[1].record()
-    torch.cuda.synchronize()
-    return ev[0].elapsed_time(ev[1]) * 1e3
 
 
-def after_bwd_gap():
-    ilu.solve_async(1, y, x)
-    ev[2].record()
-    torch.cuda._sleep(20000)
-    ev[0].record()
-    dv.spmv_dev(plan.permuted, b, sy)
-    ev[1].record()
-    torch.cuda.synchronize()
-    return ev[0].elapsed_time(ev[1]) * 1e3
+def bwd_spmv():
+    bwd()
+    spmv()
 
 
-print({"spmv_b2b_us": med(b2b), "spmv_after_bwd_us": med(after_bwd),
-       "spmv_after_bwd_and_sleep_us": med(after_bwd_gap), "bwd_impl_region": ilu._region_for("bwd") is not None})
+t_b2b = med(lambda: span(spmv))
+t_bwd = med(lambda: span(bwd))
+t_pair = med(lambda: span(bwd_spmv))
+print({"spmv_b2b_us": round(t_b2b, 2), "spmv_after_bwd_us": round(t_pair - t_bwd, 2),
+       "bwd_us": round(t_bwd, 2), "impl": os.environ.get("JV_SPMV_IMPL"),
+       "cfg": os.environ.get("JV_SPMV_CFG")})
