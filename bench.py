@@ -571,7 +571,9 @@ def run_mine(args):
                        "factor_dram_bytes"),
         "stri": roof(ab["stri"], st_avg, fdepth + bdepth,
                      f"fwd {impl['fwd']} + bwd {impl['bwd']}", "stri_dram_bytes"),
-        "spmv": roof(ab["spmv"], sp_avg, 0, "spmv_stream_kernel", "spmv_dram_bytes"),
+        "spmv": roof(ab["spmv"], sp_avg, 0,
+                     "spmv_bulk_kernel" if plan.permuted.nnz >= (1 << 20) else "spmv_stream_kernel",
+                     "spmv_dram_bytes"),
     }
     if tail is not None:
         tail_nnz = int(dv.host_i64(ilu.row_start[plan.n_upper:], 1)[0])

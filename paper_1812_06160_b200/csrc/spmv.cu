@@ -171,8 +171,8 @@ JV_INLINE void sp_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b, 
       ::"r"(sp_sa(dst)), "l"(src), "r"(bytes), "r"(sp_sa(b)), "l"(pol) : "memory");
 }
 
-template <int T, int S, int NT>
-__global__ void __launch_bounds__(NT) spmv_bulk_kernel(
+template <int T, int S, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) spmv_bulk_kernel(
     int n, int nnz, int ntiles, int tpc, int staged, const int32_t* __restrict__ rs,
     const int32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const int2* __restrict__ plan,
@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(NT) spmv_bulk_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto is_full = [&](int j) { return staged && (long long)(kb + j + 1) * T <= nnz; };
+  const int nfull = staged ? nnz / T - kb : 0;   // the CTA's tiles j < nfull arrive by bulk copy
+  auto is_full = [&](int j) { return j < nfull; };
   auto issue = [&](int j) {   // thread 0: fetch the CTA's j-th tile into its ring stage
     if (!is_full(j)) return;
     const long long p = (long long)(kb + j) * T;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(NT) spmv_bulk_kernel(
   if (tid == 0)
     for (int j = 0; j < S && j < nt; ++j) issue(j);
 
-  int2 f0 = first_row(kb), f1 = first_row(kb + 1);
+  int2 f0 = first_row(kb), f1 = first_row(kb + 1), f2 = first_row(kb + 2);
   // a row running into the CTA's first tile: fold its earlier entries
   {
     const int ts0 = kb * T;
@@ -267,14 +268,14 @@ __global__ void __launch_bounds__(NT) spmv_bulk_kernel(
     __syncthreads();
     // the tile's ring stage is free: refill it; then the next tile's gathers and row bounds
     if (tid == 0 && j + S < nt) issue(j + S);
-    const int2 f2 = first_row(k + 2);
+    const int2 f3 = first_row(k + 3);              // used two tiles on: never waited for
     const int rl = f1.x - 1;                       // last row starting in this tile
     const int rcn = f1.x - (f1.y > te ? 1 : 0);    // first row ending in the next tile
     const int rn0 = rcn + tid;
     int rna = 0, rnb = 0;
     if (j + 1 < nt) {
-      gather(j + 1);
       if (rn0 < f2.x) { rna = __ldg(rs + rn0); rnb = __ldg(rs + rn0 + 1); }
+      gather(j + 1);
     }
     const double cin = sm.carry[j & 1];
     for (int r = r0; r <= rl; r += NT) {
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(NT) spmv_bulk_kernel(
       }
     }
     f1 = f2;
+    f2 = f3;
     rc = rcn;
     r0 = rn0;
     ra = rna;
@@ -304,17 +306,17 @@ __global__ void __launch_bounds__(NT) spmv_bulk_kernel(
 
 int g_spmv_impl = -1;   // -1 auto, 0 stream, 1 bulk
 
-template <int M, int S, int NT>
+template <int M, int S, int NT, int MINB = 1>
 void spmv_bulk_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const double* val,
                       const double* x, double* y, const int32_t* tile_rows,
                       const int32_t* row_map, cudaStream_t st) {
   constexpr int T = M * kTile;
   using Sm = BulkSmem<T, S, NT>;
   static int resident = [] {
-    cudaFuncSetAttribute(spmv_bulk_kernel<T, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(spmv_bulk_kernel<T, S, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(Sm));
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_bulk_kernel<T, S, NT>, NT,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_bulk_kernel<T, S, NT, MINB>, NT,
                                                   sizeof(Sm));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -326,7 +328,7 @@ void spmv_bulk_launch(int n, int nnz, const int32_t* rs, const int32_t* col, con
   const int grid = (ntiles + tpc - 1) / tpc;
   const int staged =
       ((reinterpret_cast<uintptr_t>(col) | reinterpret_cast<uintptr_t>(val)) & 15) == 0;
-  spmv_bulk_kernel<T, S, NT><<<grid, NT, sizeof(Sm), st>>>(
+  spmv_bulk_kernel<T, S, NT, MINB><<<grid, NT, sizeof(Sm), st>>>(
       n, nnz, ntiles, tpc, staged, rs, col, val, x, y, reinterpret_cast<const int2*>(tile_rows),
       row_map);
 }
@@ -351,15 +353,13 @@ void spmv_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const do
     return;
   }
 #define JV_SPMV_ARGS n, nnz, rs, col, val, x, y, tile_rows, row_map, st
+  // ring shape (tile = M*kTile, S stages, threads, CTAs/SM the registers are bounded for);
+  // c2 in step: <2,2,256> 48.4 us, <1,2,128> 48.6, <2,3,256> 54.8, <2,2,128> 52.7 — a deeper
+  // ring costs L1 (the x gathers' cache) more than its extra bytes in flight gain
   switch (cfg) {
-    case 1: spmv_bulk_launch<2, 2, 256>(JV_SPMV_ARGS); break;
-    case 2: spmv_bulk_launch<1, 3, 128>(JV_SPMV_ARGS); break;
-    case 3: spmv_bulk_launch<1, 4, 128>(JV_SPMV_ARGS); break;
-    case 4: spmv_bulk_launch<1, 2, 256>(JV_SPMV_ARGS); break;
-    case 5: spmv_bulk_launch<1, 3, 256>(JV_SPMV_ARGS); break;
-    case 6: spmv_bulk_launch<2, 3, 256>(JV_SPMV_ARGS); break;
-    case 7: spmv_bulk_launch<2, 2, 512>(JV_SPMV_ARGS); break;
-    default: spmv_bulk_launch<1, 2, 128>(JV_SPMV_ARGS); break;
+    case 1: spmv_bulk_launch<1, 2, 128, 9>(JV_SPMV_ARGS); break;
+    case 2: spmv_bulk_launch<2, 3, 256, 4>(JV_SPMV_ARGS); break;
+    default: spmv_bulk_launch<2, 2, 256, 4>(JV_SPMV_ARGS); break;
   }
 #undef JV_SPMV_ARGS
 }

@@ -146,3 +146,51 @@ def test_factor_parallel_upper_row_runs(runs):
                            oracle._p(norms), 0.0, 0, lo, hi, 0, a.n)
     jv.factor_parallel_upper(f, sched)
     assert np.array_equal(f.val, want)
+
+
+def test_spmv_keeps_the_matrix_resident(uploads, rng):
+    """The reference's Krylov loop calls spmv(a, p) per iteration
+    (krylov.py:52-151): the matrix is uploaded once, and again only after
+    the caller could have changed it."""
+    a = jv.poisson2d(24)
+    rs, col, val = a.row_start.astype(np.int64), a.col.astype(np.int64), a.val.copy()
+    uploads.clear()
+    xs = [rng.uniform(-1, 1, a.n) for _ in range(4)]
+    for x in xs:
+        assert np.array_equal(jv.spmv(a, x), oracle.spmv(rs, col, val, x))
+    assert len(uploads) == 1, uploads           # (the a.val read above came first)
+    a.val[:] *= 2.0                             # in-place edit through the attribute
+    assert np.array_equal(jv.spmv(a, xs[0]), oracle.spmv(rs, col, 2.0 * val, xs[0]))
+    assert len(uploads) == 2
+    alias = a.val                               # a kept alias: never trusted
+    jv.spmv(a, xs[0])
+    alias[0] = 7.0
+    val2 = 2.0 * val
+    val2[0] = 7.0
+    assert np.array_equal(jv.spmv(a, xs[1]), oracle.spmv(rs, col, val2, xs[1]))
+    a.val = val.copy()                          # rebinding
+    del alias
+    assert np.array_equal(jv.spmv(a, xs[2]), oracle.spmv(rs, col, val, xs[2]))
+    n_up = len(uploads)
+    assert np.array_equal(jv.spmv(a, xs[3]), oracle.spmv(rs, col, val, xs[3]))
+    assert len(uploads) == n_up
+
+
+def test_long_vectors_come_back_in_pinned_memory(rng):
+    """Results of the drop-in solves of at least 2^17 entries are written by
+    one DMA into page-locked memory; the caller owns the array."""
+    from paper_1812_06160_b200 import workloads as W
+
+    a = W.laplace7(52)                           # 140,608 rows
+    f = jv.assemble_factors(a, jv.ilu0_pattern(a.pattern), jv.Permutation.identity(a.n))
+    jv.factor_serial(f)
+    vals = f.val.copy()
+    r = rng.uniform(-1, 1, a.n)
+    z = jv.apply_preconditioner(f, r)
+    assert z.flags.writeable and z.dtype == np.float64 and z.shape == (a.n,)
+    assert np.array_equal(z, expected_apply(f, vals, r))
+    keep = z.copy()
+    z2 = jv.apply_preconditioner(f, 2.0 * r)     # a second result must not alias the first
+    assert np.array_equal(z, keep) and not np.shares_memory(z, z2)
+    with pytest.raises(ValueError):
+        jv.apply_preconditioner(f, r[:-1])
