@@ -92,8 +92,11 @@ int jv_test_ddiv(int32_t n, const double* a, const double* b, double* out, void*
  * Two kernels, same bits: a CTA-per-tile stream kernel (small matrices)
  * and a persistent kernel whose col/val tiles arrive by bulk copies (TMA)
  * in a shared-memory ring (from 2^20 nonzeros; col and val 16-byte
- * aligned, else its tiles are loaded directly).  jv_set_spmv_impl: -1 by
- * size (default), 0 stream, 1 persistent.
+ * aligned, else its tiles are loaded directly; not for matrices with rows
+ * spanning two whole tiles — power-law hubs — whose serial sums the
+ * CTA-per-tile kernel spreads better: jv_spmv_plan notes that per plan
+ * pointer and synchronises the stream once to do so).  jv_set_spmv_impl:
+ * -1 by size and plan (default), 0 stream, 1 persistent.
  * tile_rows (nullable) is the jv_spmv_plan output, int32[2*(ntiles+1)]
  * (first row of each tile boundary and that row's first nonzero) with
  * ntiles = max(1, ceil(nnz / jv_spmv_tile())).                           */

@@ -13,6 +13,9 @@
 // has its products formed by the whole CTA chunk by chunk and summed by one
 // thread in order, so it is bitwise too.  The tile -> first-row map is a setup-time plan
 // (jv_spmv_plan); without it each CTA binary-searches row_start.
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "../../include/jv.h"
 
@@ -306,6 +309,21 @@ __global__ void __launch_bounds__(NT, MINB) spmv_bulk_kernel(
 
 int g_spmv_impl = -1;   // -1 auto, 0 stream, 1 bulk
 
+// plan pointer -> "has rows spanning kLongRun whole tiles" (jv_spmv_plan)
+std::mutex g_spmv_mu;
+std::unordered_map<const void*, bool> g_spmv_long;
+constexpr int kLongRun = 2;
+
+// longest run of consecutive tiles in which no row starts (capped at 64)
+__global__ void spmv_plan_stat_kernel(int ntiles, const int32_t* tile_rows, int* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles || tile_rows[2 * t] != tile_rows[2 * t + 2]) return;
+  if (t > 0 && tile_rows[2 * t - 2] == tile_rows[2 * t]) return;   // not the run's first tile
+  int r = 1;
+  while (r < 64 && t + r < ntiles && tile_rows[2 * (t + r)] == tile_rows[2 * (t + r) + 2]) ++r;
+  atomicMax(out, r);
+}
+
 template <int M, int S, int NT, int MINB = 1>
 void spmv_bulk_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const double* val,
                       const double* x, double* y, const int32_t* tile_rows,
@@ -345,7 +363,12 @@ void spmv_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const do
     return e ? atoi(e) : 0;
   }();
   const int impl = g_spmv_impl >= 0 ? g_spmv_impl : env;
-  const bool bulk = tile_rows != nullptr && nnz > 0 && (impl == 1 || (impl < 0 && nnz >= (1 << 20)));
+  bool bulk = tile_rows != nullptr && nnz > 0 && (impl == 1 || (impl < 0 && nnz >= (1 << 20)));
+  if (bulk && impl < 0) {
+    std::lock_guard<std::mutex> lock(g_spmv_mu);
+    auto it = g_spmv_long.find(tile_rows);
+    if (it != g_spmv_long.end() && it->second) bulk = false;
+  }
   if (!bulk) {
     const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
     spmv_stream_kernel<<<ntiles, kSpmvThreads, 0, st>>>(n, nnz, rs, col, val, x, y, tile_rows,
@@ -375,9 +398,23 @@ extern "C" int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, in
                             void* stream) {
   if (n < 0 || nnz < 0) { jvh::set_error("jv_spmv_plan: bad size"); return JV_EINVAL; }
   const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
-  spmv_plan_kernel<<<(ntiles + 256) / 256, 256, 0, (cudaStream_t)stream>>>(n, nnz, ntiles,
-                                                                          row_start, tile_rows);
+  cudaStream_t st = (cudaStream_t)stream;
+  spmv_plan_kernel<<<(ntiles + 256) / 256, 256, 0, st>>>(n, nnz, ntiles, row_start, tile_rows);
   JV_CHECK_LAUNCH("jv_spmv_plan");
+  // Rows spanning whole tiles (power-law hubs): their serial sums stall a
+  // persistent CTA's whole tile range, while the CTA-per-tile kernel spreads
+  // them over the GPU — remember which kernel this plan's matrix wants.
+  // (Setup call: synchronises the stream once.)
+  std::lock_guard<std::mutex> lock(g_spmv_mu);
+  int run = 0;
+  int* drun = nullptr;
+  if (cudaMallocAsync(&drun, sizeof(int), st) != cudaSuccess) { cudaGetLastError(); return JV_OK; }
+  cudaMemsetAsync(drun, 0, sizeof(int), st);
+  spmv_plan_stat_kernel<<<(ntiles + 255) / 256, 256, 0, st>>>(ntiles, tile_rows, drun);
+  cudaMemcpyAsync(&run, drun, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(drun, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) { cudaGetLastError(); return JV_OK; }
+  g_spmv_long[tile_rows] = run >= kLongRun;
   return JV_OK;
 }
 

@@ -13,8 +13,8 @@ for c in c2 c1 c3 c4 c5; do
   python tools/bench_brief.py gpurun_out/r02_bench_${c}_$TAG.json
 done
 # launch list of the same command (cold-cache, serialised: shares only)
-ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
-  --log-file gpurun_out/r02_launches_c2_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/r02_launches_c2_$TAG.csv python bench.py --steps 4 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
 python tools/ncu_summary.py launches gpurun_out/r02_launches_c2_$TAG.csv > gpurun_out/r02_launches_c2_$TAG.txt
 head -14 gpurun_out/r02_launches_c2_$TAG.txt
 # one step per config under ncu --set full
