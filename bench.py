@@ -574,7 +574,8 @@ def run_mine(args):
         "stri": roof(ab["stri"], st_avg, fdepth + bdepth,
                      f"fwd {impl['fwd']} + bwd {impl['bwd']}", "stri_dram_bytes"),
         "spmv": roof(ab["spmv"], sp_avg, 0,
-                     "spmv_bulk_kernel" if plan.permuted.nnz >= (1 << 20) else "spmv_stream_kernel",
+                     "spmv_bulk_kernel" if _L.load().jv_spmv_impl_for(
+                         plan.permuted.nnz, dv.ptr(plan.permuted.tile_rows())) else "spmv_stream_kernel",
                      "spmv_dram_bytes"),
     }
     if tail is not None:
@@ -695,7 +696,7 @@ def measure_e2e(a, plan, args):
     assembled = dv.host_f64(plan.assembled, ilu.nnz)
     f = IluFactors(n, pat, assembled.copy(), dv.host_i64(ilu.diag_pos, n),
                    jv.Permutation(dv.host_i64(plan.perm, n)), ilu.tau, ilu.milu)
-    for _ in range(2):
+    for _ in range(4):   # factor_serial times whole vs streamed transfers on its first four calls
         f.val[:] = assembled
         jv.factor_serial(f)
     ts = []

@@ -102,6 +102,7 @@ int jv_test_ddiv(int32_t n, const double* a, const double* b, double* out, void*
  * ntiles = max(1, ceil(nnz / jv_spmv_tile())).                           */
 int jv_spmv_tile(void);
 int jv_set_spmv_impl(int impl);
+int jv_spmv_impl_for(int32_t nnz, const int32_t* tile_rows);   /* 1 persistent, 0 stream */
 int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, int32_t* tile_rows,
                  void* stream);
 int jv_spmv(int32_t n, int32_t nnz, const int32_t* row_start, const int32_t* col,

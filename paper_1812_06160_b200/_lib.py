@@ -42,6 +42,7 @@ _SIGS = {
     "jv_test_ddiv": [c_int32, _P, _P, _P, _P],
     "jv_spmv_tile": [],
     "jv_set_spmv_impl": [c_int],
+    "jv_spmv_impl_for": [c_int32, _P],
     "jv_spmv_plan": [c_int32, c_int32, _P, _P, _P],
     "jv_spmv": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P],
     "jv_spmv_rows": [c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -351,16 +351,10 @@ void spmv_bulk_launch(int n, int nnz, const int32_t* rs, const int32_t* col, con
       row_map);
 }
 
-void spmv_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const double* val,
-                 const double* x, double* y, const int32_t* tile_rows, const int32_t* row_map,
-                 cudaStream_t st) {
+bool spmv_use_bulk(int nnz, const int32_t* tile_rows) {
   static const int env = [] {
     const char* e = getenv("JV_SPMV_IMPL");
     return e ? atoi(e) : -1;
-  }();
-  static const int cfg = [] {
-    const char* e = getenv("JV_SPMV_CFG");   // tuning: ring depth / threads of the bulk kernel
-    return e ? atoi(e) : 0;
   }();
   const int impl = g_spmv_impl >= 0 ? g_spmv_impl : env;
   bool bulk = tile_rows != nullptr && nnz > 0 && (impl == 1 || (impl < 0 && nnz >= (1 << 20)));
@@ -369,6 +363,17 @@ void spmv_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const do
     auto it = g_spmv_long.find(tile_rows);
     if (it != g_spmv_long.end() && it->second) bulk = false;
   }
+  return bulk;
+}
+
+void spmv_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const double* val,
+                 const double* x, double* y, const int32_t* tile_rows, const int32_t* row_map,
+                 cudaStream_t st) {
+  static const int cfg = [] {
+    const char* e = getenv("JV_SPMV_CFG");   // tuning: ring depth / threads of the bulk kernel
+    return e ? atoi(e) : 0;
+  }();
+  const bool bulk = spmv_use_bulk(nnz, tile_rows);
   if (!bulk) {
     const int ntiles = nnz > 0 ? (nnz + kTile - 1) / kTile : 1;
     spmv_stream_kernel<<<ntiles, kSpmvThreads, 0, st>>>(n, nnz, rs, col, val, x, y, tile_rows,
@@ -393,6 +398,10 @@ extern "C" int jv_spmv_tile(void) { return kTile; }
 
 // -1: by size (bulk from 2^20 nonzeros), 0: CTA-per-tile stream kernel, 1: persistent bulk kernel
 extern "C" int jv_set_spmv_impl(int impl) { g_spmv_impl = impl; return JV_OK; }
+// 1 when jv_spmv would run the persistent kernel for this matrix and plan, else 0
+extern "C" int jv_spmv_impl_for(int32_t nnz, const int32_t* tile_rows) {
+  return spmv_use_bulk(nnz, tile_rows) ? 1 : 0;
+}
 
 extern "C" int jv_spmv_plan(int32_t n, int32_t nnz, const int32_t* row_start, int32_t* tile_rows,
                             void* stream) {

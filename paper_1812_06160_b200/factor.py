@@ -11,6 +11,9 @@ kernel has quiesced (factor.py:61-63).
 
 from __future__ import annotations
 
+import os
+import time
+
 import numpy as np
 
 from . import device as dv
@@ -70,18 +73,49 @@ def factor_serial(factors: IluFactors) -> None:
     if (factors.pattern.nnz * 8 >= dv.STREAM_MIN_BYTES and not factors.device_is_current()
             and dv.pinned_host(host)):
         # large page-locked host values: upload, factorization and download
-        # overlap chunk by chunk (DevIlu.factor_streamed)
+        # can overlap chunk by chunk (DevIlu.factor_streamed).  The chunked
+        # sweeps run the sync-free kernel per row range, which for some
+        # patterns costs more than the overlap saves (config 3: 19 vs 8 ms),
+        # so both ways are timed once per pattern and the faster one kept
+        # (identical results).
         d = factors.device()
-        bad = d.factor_streamed(host)
-        d.holder = factors
-        if bad < 0:
-            factors._synced()
+        mode = _stream_mode(d)
+        t0 = time.perf_counter()
+        if mode == "streamed":
+            bad = d.factor_streamed(host)
+            d.holder = factors
+            if bad < 0:
+                factors._synced()
+            else:
+                factors._dirty = True
         else:
-            factors._dirty = True
+            bad = _run(factors, keep_after_bad=True)
+        _stream_note(d, mode, time.perf_counter() - t0)
     else:
         bad = _run(factors, keep_after_bad=True)
     if bad >= 0:
         raise ZeroPivotError(int(bad))
+
+
+# calls 1-2 whole (the first builds schedules), 3-4 streamed (the third builds
+# the chunk schedules); from the fifth call on the faster of calls 2 and 4
+_STREAM_PLAN = ("whole", "whole", "streamed", "streamed")
+
+
+def _stream_mode(d) -> str:
+    forced = os.environ.get("JV_STREAM")           # "0" whole, "1" streamed
+    if forced in ("0", "1"):
+        return "streamed" if forced == "1" else "whole"
+    hist = d.__dict__.setdefault("_stream_hist", [])
+    if len(hist) < len(_STREAM_PLAN):
+        return _STREAM_PLAN[len(hist)]
+    return "streamed" if hist[3] < hist[1] else "whole"
+
+
+def _stream_note(d, mode: str, seconds: float) -> None:
+    hist = d.__dict__.setdefault("_stream_hist", [])
+    if len(hist) < len(_STREAM_PLAN):
+        hist.append(seconds)
 
 
 def _row_runs(rows: np.ndarray):

@@ -55,19 +55,27 @@ def _factor_case(n_side=40, zero_row=None):
     return jv, jv.assemble_factors(a, pat, jv.Permutation.identity(a.n))
 
 
+@pytest.mark.parametrize("forced", ["1", None])
 @pytest.mark.parametrize("zero_row", [None, 700])
-def test_streamed_factor_serial(monkeypatch, zero_row):
+def test_streamed_factor_serial(monkeypatch, zero_row, forced):
     """The chunked upload / factor / download pipeline of factor_serial
     (DevIlu.factor_streamed) gives the serial oracle's bits, and after a zero
-    pivot the later rows hold their input values (the reference stops)."""
+    pivot the later rows hold their input values (the reference stops).
+    forced "1": every call streamed; None: the API's own schedule — two
+    whole calls, two streamed, then the faster of the two (six calls cover
+    all three)."""
     import oracle
     jv, f = _factor_case(zero_row=zero_row)
     monkeypatch.setattr(dv, "STREAM_MIN_BYTES", 0)
     monkeypatch.setattr(dv, "_REG_MIN", 0)
+    if forced is None:
+        monkeypatch.delenv("JV_STREAM", raising=False)
+    else:
+        monkeypatch.setenv("JV_STREAM", forced)
     f.val = np.array(f.val, copy=True)        # an owning array, page-locked by the API
     before = f.val.copy()
     want, wbad = oracle.factor_serial(f.pattern.row_start, f.pattern.col, before, f.diag_pos)
-    for _ in range(2):
+    for _ in range(2 if forced else 6):
         f.val[:] = before
         if wbad < 0:
             jv.factor_serial(f)
