@@ -180,6 +180,15 @@ int jv_check_diagonal(int32_t n, const int32_t* row_start, const int32_t* col,
 int jv_iluk1_pattern(int32_t n, const int32_t* row_start, const int32_t* col,
                      int32_t* out_row_start, int32_t* out_col, int32_t* out_lev,
                      int64_t* nnz_h, void* stream);
+/* ILU(k >= 2): one round of the level-of-fill closure on a levelled pattern
+ * (symbolic.py:86-138): every strict-lower entry (m, a) of row i with every
+ * strict-upper entry (j, b) of row m gives (j, a + b + 1) when that is <= K;
+ * per column the smallest level wins.  K rounds from (A, level 0) give the
+ * reference's ILU(K) pattern and level table.  Two-call protocol like
+ * jv_iluk1_pattern (out_col NULL: only out_row_start and *nnz_h).          */
+int jv_iluk_round(int32_t n, const int32_t* row_start, const int32_t* col, const int32_t* lev,
+                  int32_t K, int32_t* out_row_start, int32_t* out_col, int32_t* out_lev,
+                  int64_t* nnz_h, void* stream);
 /* Values of the (already permuted) matrix into the factor pattern; fill
  * positions start at 0; diag_pos found; uncovered entries -> *bad_cover,
  * missing diagonals -> *bad_diag (both atomicMin rows).  symbolic.py:146-181 */

@@ -55,6 +55,7 @@ _SIGS = {
     "jv_permute_symmetric": [c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "jv_check_diagonal": [c_int32, _P, _P, _P, _P],
     "jv_iluk1_pattern": [c_int32, _P, _P, _P, _P, _P, POINTER(c_int64), _P],
+    "jv_iluk_round": [c_int32, _P, _P, _P, c_int32, _P, _P, _P, POINTER(c_int64), _P],
     "jv_assemble": [c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "jv_row_norms": [c_int32, _P, _P, c_double, _P, _P],
     "jv_rcm_host": [c_int32, _P, _P, _P],

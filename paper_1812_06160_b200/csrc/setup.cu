@@ -682,6 +682,157 @@ extern "C" int jv_iluk1_pattern(int32_t n, const int32_t* row_start, const int32
   return JV_OK;
 }
 
+// ---------------------------------------------------- ILU(k) symbolic, k >= 2
+// One round of the level-of-fill closure (symbolic.py:86-138) on a levelled
+// pattern: row i keeps its entries and gains (j, a + b + 1) for every strict-
+// lower entry (m, a) of row i and strict-upper entry (j, b) of row m with
+// a + b + 1 <= K; per column the smallest level wins.  Levels are exact by
+// induction on their value — an entry of level l needs a pair of levels
+// summing to l - 1, all present after l - 1 rounds — so K rounds from
+// (A, level 0) give the reference's ILU(K) pattern and level table.
+// Candidates are 64-bit keys (column << 8 | level), segment-sorted per row;
+// pairs over the level bound are written as a sentinel that sorts last.
+namespace {
+constexpr unsigned long long kIlukSent = ~0ull;
+
+__global__ void ilukr_bound_kernel(int n, const int32_t* rs, const int32_t* col,
+                                   const int32_t* lev, int K, long long* bound) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    long long b = rs[i + 1] - rs[i];
+    for (int p = rs[i]; p < rs[i + 1]; ++p) {
+      const int m = col[p];
+      if (m >= i) break;
+      if (lev[p] >= K) continue;
+      int lo = rs[m], hi = rs[m + 1];
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (col[mid] <= m) lo = mid + 1; else hi = mid;
+      }
+      b += rs[m + 1] - lo;
+    }
+    bound[i] = b;
+  }
+}
+
+__global__ void ilukr_fill_kernel(int n, const int32_t* rs, const int32_t* col,
+                                  const int32_t* lev, int K, const long long* boff,
+                                  unsigned long long* cand) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    long long o = boff[i];
+    const int a = rs[i], b = rs[i + 1];
+    for (int t = lane; t < b - a; t += 32)
+      cand[o + t] = ((unsigned long long)(unsigned)col[a + t] << 8) | (unsigned)lev[a + t];
+    o += b - a;
+    for (int p = a; p < b; ++p) {
+      const int m = col[p];
+      if (m >= i) break;
+      const int la = lev[p];
+      if (la >= K) continue;
+      int lo = rs[m], hi = rs[m + 1];
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (col[mid] <= m) lo = mid + 1; else hi = mid;
+      }
+      for (int t = lane; t < rs[m + 1] - lo; t += 32) {
+        const int l = la + lev[lo + t] + 1;
+        cand[o + t] = l <= K ? ((unsigned long long)(unsigned)col[lo + t] << 8) | (unsigned)l
+                             : kIlukSent;
+      }
+      o += rs[m + 1] - lo;
+    }
+  }
+}
+
+__global__ void ilukr_count_kernel(int n, const long long* boff, const unsigned long long* cand,
+                                   int32_t* cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int k = 0;
+    for (long long p = boff[i]; p < boff[i + 1]; ++p) {
+      if (cand[p] == kIlukSent) break;
+      if (p == boff[i] || (cand[p] >> 8) != (cand[p - 1] >> 8)) ++k;
+    }
+    cnt[i] = k;
+  }
+}
+
+__global__ void ilukr_emit_kernel(int n, const long long* boff, const unsigned long long* cand,
+                                  const int32_t* ors, int32_t* ocol, int32_t* olev) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int o = ors[i];
+    for (long long p = boff[i]; p < boff[i + 1]; ++p) {
+      if (cand[p] == kIlukSent) break;
+      if (p != boff[i] && (cand[p] >> 8) == (cand[p - 1] >> 8)) continue;
+      ocol[o] = (int32_t)(cand[p] >> 8);      // first of its column: the smallest level
+      olev[o] = (int32_t)(cand[p] & 0xff);
+      ++o;
+    }
+  }
+}
+}  // namespace
+
+extern "C" int jv_iluk_round(int32_t n, const int32_t* row_start, const int32_t* col,
+                             const int32_t* lev, int32_t K, int32_t* out_row_start,
+                             int32_t* out_col, int32_t* out_lev, int64_t* nnz_h, void* stream) {
+  // Called twice like jv_iluk1_pattern: out_col == NULL sizes the result.
+  cudaStream_t s = (cudaStream_t)stream;
+  if (K < 1 || K > 254) { jvh::set_error("jv_iluk_round: fill level out of range"); return JV_EINVAL; }
+  if (n == 0) { set_int_kernel<<<1, 1, 0, s>>>(out_row_start, 0); *nnz_h = 0; return JV_OK; }
+  Tmp bound(s), boff(s), cand(s), sorted(s), cnt(s), tmp(s);
+  CK_CUDA(bound.alloc(sizeof(long long) * (n + 1)), "alloc");
+  CK_CUDA(boff.alloc(sizeof(long long) * (n + 1)), "alloc");
+  ilukr_bound_kernel<<<grid_for(n), kSetupThreads, 0, s>>>(n, row_start, col, lev, K,
+                                                           (long long*)bound.p);
+  CK_CUDA(cudaMemsetAsync((long long*)bound.p + n, 0, sizeof(long long), s), "memset");
+  size_t tb = 0;
+  CK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long*)bound.p, (long long*)boff.p, n + 1, s),
+          "scan size");
+  CK_CUDA(tmp.alloc(tb), "alloc");
+  CK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, (long long*)bound.p, (long long*)boff.p, n + 1, s),
+          "scan");
+  long long total = 0;
+  CK_CUDA(cudaMemcpyAsync(&total, (long long*)boff.p + n, sizeof(long long), cudaMemcpyDeviceToHost, s),
+          "copy");
+  CK_CUDA(cudaStreamSynchronize(s), "sync");
+  if (total >= (1LL << 31)) { jvh::set_error("jv_iluk_round: candidate list too large"); return JV_ENOMEM; }
+  CK_CUDA(cand.alloc(sizeof(unsigned long long) * total), "alloc");
+  CK_CUDA(sorted.alloc(sizeof(unsigned long long) * total), "alloc");
+  ilukr_fill_kernel<<<grid_for((long long)n * 32), kSetupThreads, 0, s>>>(
+      n, row_start, col, lev, K, (const long long*)boff.p, (unsigned long long*)cand.p);
+  size_t tb2 = 0;
+  CK_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb2, (const unsigned long long*)cand.p,
+                                             (unsigned long long*)sorted.p, (int)total, n,
+                                             (const long long*)boff.p, (const long long*)boff.p + 1, s),
+          "segsort size");
+  Tmp tmp2(s);
+  CK_CUDA(tmp2.alloc(tb2), "alloc");
+  CK_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp2.p, tb2, (const unsigned long long*)cand.p,
+                                             (unsigned long long*)sorted.p, (int)total, n,
+                                             (const long long*)boff.p, (const long long*)boff.p + 1, s),
+          "segsort");
+  CK_CUDA(cnt.alloc(sizeof(int32_t) * (n + 1)), "alloc");
+  ilukr_count_kernel<<<grid_for(n), kSetupThreads, 0, s>>>(
+      n, (const long long*)boff.p, (const unsigned long long*)sorted.p, (int32_t*)cnt.p);
+  set_int_kernel<<<1, 1, 0, s>>>((int32_t*)cnt.p + n, 0);
+  size_t tb3 = 0;
+  CK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb3, (int32_t*)cnt.p, out_row_start, n + 1, s),
+          "scan size");
+  Tmp tmp3(s);
+  CK_CUDA(tmp3.alloc(tb3), "alloc");
+  CK_CUDA(cub::DeviceScan::ExclusiveSum(tmp3.p, tb3, (int32_t*)cnt.p, out_row_start, n + 1, s), "scan");
+  int32_t nz = 0;
+  CK_CUDA(cudaMemcpyAsync(&nz, out_row_start + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s), "copy");
+  CK_CUDA(cudaStreamSynchronize(s), "sync");
+  *nnz_h = nz;
+  if (out_col)
+    ilukr_emit_kernel<<<grid_for(n), kSetupThreads, 0, s>>>(
+        n, (const long long*)boff.p, (const unsigned long long*)sorted.p, out_row_start, out_col,
+        out_lev);
+  JV_CHECK_LAUNCH("jv_iluk_round");
+  return JV_OK;
+}
+
 extern "C" int jv_assemble(int32_t n, const int32_t* a_row_start, const int32_t* a_col,
                            const double* a_val, const int32_t* f_row_start, const int32_t* f_col,
                            double* f_val, int32_t* diag_pos, int32_t* bad_cover, int32_t* bad_diag,

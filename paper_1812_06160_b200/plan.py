@@ -82,13 +82,9 @@ def build_plan(a: CsrMatrix, base_perm=None, k: int = 0, tau: float = 0.0, milu:
     elif k == 1:
         fpat, fill = iluk1_dev(permuted)
     else:
-        from .symbolic import iluk_pattern
-        from .csr import SparsityPattern
+        from .symbolic import iluk_dev
 
-        rs, col = permuted.host_pattern()
-        p, table = iluk_pattern(SparsityPattern(n, rs, col), k)
-        fpat = dv.DevCsr.from_host(n, p.row_start, p.col)
-        fill = dv.i32(table.level)
+        fpat, fill = iluk_dev(permuted, k)      # k rounds of jv_iluk_round, all in HBM
     val, diag, bad_cover, bad_diag = assemble_dev(permuted, fpat)
     if bad_cover >= 0:
         raise MatrixFormatError("pattern does not cover the permuted matrix")

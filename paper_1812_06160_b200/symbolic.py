@@ -157,6 +157,32 @@ def iluk1_dev(d: dv.DevCsr, want_levels: bool = True):
     return dv.DevCsr(d.n, int(nnz.value), out_rs, out_col), out_lev
 
 
+def iluk_dev(d: dv.DevCsr, k: int):
+    """ILU(k) pattern and fill levels on the device for any k >= 1: k rounds
+    of the level-of-fill closure (jv_iluk_round) from (A, level 0).  Levels
+    are exact by induction on their value, so the result is the reference's
+    row-by-row symbolic factorization (symbolic.py:86-138).  Returns
+    (DevCsr, int32 level tensor)."""
+    t = dv.torch()
+    cur = d
+    lev = t.zeros(max(d.nnz, 1), dtype=t.int32, device="cuda")
+    for _ in range(k):
+        out_rs = dv.empty_i32(d.n + 1)
+        nnz = ctypes.c_int64(0)
+        args = (d.n, dv.ptr(cur.row_start), dv.ptr(cur.col), dv.ptr(lev), int(k), dv.ptr(out_rs))
+        _lib.call("jv_iluk_round", *args, None, None, ctypes.byref(nnz), dv.stream())
+        out_col = dv.empty_i32(nnz.value)
+        out_lev = dv.empty_i32(nnz.value)
+        _lib.call("jv_iluk_round", *args, dv.ptr(out_col), dv.ptr(out_lev), ctypes.byref(nnz),
+                  dv.stream())
+        grown = int(nnz.value) != cur.nnz
+        same = (not grown) and bool(t.equal(out_lev[:cur.nnz], lev[:cur.nnz]))
+        cur, lev = dv.DevCsr(d.n, int(nnz.value), out_rs, out_col), out_lev
+        if same:
+            break          # fixed point before round k: nothing more can appear
+    return cur, lev
+
+
 def iluk_pattern(pattern: SparsityPattern, k: int) -> tuple[SparsityPattern, FillLevelTable]:
     """Level-of-fill symbolic factorization (symbolic.py:86-138)."""
     if k < 0:
@@ -173,7 +199,22 @@ def iluk_pattern(pattern: SparsityPattern, k: int) -> tuple[SparsityPattern, Fil
         out, lev = iluk1_dev(d)
         rs, col = out.host_pattern()
         return SparsityPattern(pattern.n, rs, col), FillLevelTable(dv.host_i64(lev, out.nnz))
-    # k >= 2: libjv host C++ (setup only; device ILU(k>=2) is the next item)
+    if k <= 254:
+        try:
+            out, lev = iluk_dev(d, k)
+        except RuntimeError as e:            # candidate lists beyond int32: host C++ below
+            if "too large" not in str(e):
+                raise
+        else:
+            rs, col = out.host_pattern()
+            return SparsityPattern(pattern.n, rs, col), FillLevelTable(dv.host_i64(lev, out.nnz))
+    return _iluk_host(pattern, k)
+
+
+def _iluk_host(pattern: SparsityPattern, k: int) -> tuple[SparsityPattern, FillLevelTable]:
+    """Row-by-row symbolic factorization in libjv's host C++ (setup; used
+    when a round's candidate lists exceed int32, and as the test oracle's
+    counterpart for the device rounds)."""
     rs = np.ascontiguousarray(pattern.row_start, dtype=np.int32)
     col = np.ascontiguousarray(pattern.col, dtype=np.int32)
     prs = ctypes.POINTER(ctypes.c_int32)()
