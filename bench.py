@@ -580,9 +580,18 @@ def run_mine(args):
     def roof(nbytes, secs, depth, kernel, traffic_key):
         a = nbytes / secs / 1e9
         return {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak,
+                "frac_of_8TBs_nominal": a / 8000.0,
                 "peak_kind": peak_kind, "alg_bytes": nbytes, "us": secs * 1e6,
                 "traffic": prof.get(traffic_key), "kernel": kernel, "dag_depth": depth,
                 "t_hop_us": t_hop_us, "depth_x_thop_us": depth * t_hop_us}
+    # tau > 0: strict-lower positions left exactly 0 by the timed factorization
+    # (dropped multipliers, fill included; full_digests.json stats.zero_l)
+    zero_l = None
+    if s["tau"] > 0 and not batched:
+        rows = torch.repeat_interleave(torch.arange(n, device="cuda"),
+                                       (ilu.row_start[1:n + 1] - ilu.row_start[:n]).long())
+        low = torch.arange(nnz_f, device="cuda") < ilu.diag_pos[:n].long()[rows]
+        zero_l = int(((ilu.val[:nnz_f] == 0.0) & low).sum().item())
     rooflines = {
         "factor": roof(ab["factor"], f_avg, fdepth,
                        {"tickets": "factor_kernel", "region": "region_kernel<0>",
@@ -650,6 +659,7 @@ def run_mine(args):
         "paths": paths,
         "e2e": e2e,
         "setup": setup,
+        "tau_zero_l": zero_l,
         "gpu_launches": launches,
         "gpu_launch_detail": launch_detail,
         "clocks": clocks,

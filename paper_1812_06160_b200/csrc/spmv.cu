@@ -286,11 +286,16 @@ __global__ void __launch_bounds__(NT, MINB) spmv_bulk_kernel(
       double s = r == rc ? cin : 0.0;
       const int qb = min(rb, te) - ts;
       int q = max(ra, ts) - ts;
-      for (; q + 4 <= qb; q += 4) {   // four loads in flight, added in order
-        const double p0 = prod[q], p1 = prod[q + 1], p2 = prod[q + 2], p3 = prod[q + 3];
-        s = jv::dadd(jv::dadd(jv::dadd(jv::dadd(s, p0), p1), p2), p3);
+      // eight loads in flight (clamped inside the tile), added in order; the
+      // predicated adds keep short rows in one pass without a remainder loop
+      for (; q < qb; q += 8) {
+        double pv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pv[i] = prod[min(q + i, T - 1)];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (q + i < qb) s = jv::dadd(s, pv[i]);
       }
-      for (; q < qb; ++q) s = jv::dadd(s, prod[q]);
       if (rb <= te) {
         __stcs(y + (row_map ? __ldg(row_map + r) : r), s);
         if (r == rl) sm.carry[(j + 1) & 1] = 0.0;
@@ -382,12 +387,13 @@ void spmv_launch(int n, int nnz, const int32_t* rs, const int32_t* col, const do
   }
 #define JV_SPMV_ARGS n, nnz, rs, col, val, x, y, tile_rows, row_map, st
   // ring shape (tile = M*kTile, S stages, threads, CTAs/SM the registers are bounded for);
-  // c2 in step: <2,2,256> 48.4 us, <1,2,128> 48.6, <2,3,256> 54.8, <2,2,128> 52.7 — a deeper
-  // ring costs L1 (the x gathers' cache) more than its extra bytes in flight gain
+  // c2 right after a sweep / back to back: <1,2,128> 47.1 / 42.7 us, <2,2,256> 49.2 / 41.5,
+  // <2,3,256> 54.8 / 45.7 — a deeper ring costs L1 (the x gathers' cache) more than its extra
+  // bytes in flight gain
   switch (cfg) {
-    case 1: spmv_bulk_launch<1, 2, 128, 9>(JV_SPMV_ARGS); break;
+    case 1: spmv_bulk_launch<2, 2, 256, 4>(JV_SPMV_ARGS); break;
     case 2: spmv_bulk_launch<2, 3, 256, 4>(JV_SPMV_ARGS); break;
-    default: spmv_bulk_launch<2, 2, 256, 4>(JV_SPMV_ARGS); break;
+    default: spmv_bulk_launch<1, 2, 128, 9>(JV_SPMV_ARGS); break;
   }
 #undef JV_SPMV_ARGS
 }
