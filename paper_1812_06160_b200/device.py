@@ -128,6 +128,11 @@ _REGION_D_CAP = int(os.environ.get("JV_REGION_D", "99"))   # diagnostics: shallo
 STREAM_MIN_BYTES = 32 << 20    # streamed factor_serial above this many value bytes
 
 
+def _is_registered(a):
+    """True when `a` is already page-locked (never registers)."""
+    return a.flags.c_contiguous and _REGISTERED.get(a.ctypes.data) == a.nbytes
+
+
 def pinned_host(a):
     """Page-lock a float64 host array in place when possible (True if so)."""
     return isinstance(a, np.ndarray) and a.dtype == np.float64 and _registered(a)
@@ -143,9 +148,10 @@ def upload_f64(dst, src):
     return _upload(dst, src, _CHUNK)
 
 
-def _upload(dst, src, chunk):
+def _upload(dst, src, chunk, register=True):
     t = torch()
-    if isinstance(src, np.ndarray) and src.dtype == np.float64 and _registered(src):
+    if (isinstance(src, np.ndarray) and src.dtype == np.float64
+            and (_registered(src) if register else _is_registered(src))):
         _lib.call("jv_memcpy_async", ptr(dst), ctypes.c_void_p(src.ctypes.data), src.nbytes, 0,
                   stream())
         sync()   # the caller may reuse its array as soon as we return
@@ -172,7 +178,10 @@ def upload_vec(src, n):
     if src.shape != (n,):
         raise ValueError(f"vector of shape {src.shape} for a system of {n} rows")
     x = empty_f64(n)
-    _upload(x, src, VEC_CHUNK)
+    # per-call vectors are usually fresh arrays: page-locking each one
+    # (cudaHostRegister, ~ms) would cost more than the staging copy, so only
+    # an array the caller already had registered takes the direct DMA
+    _upload(x, src, VEC_CHUNK, register=False)
     return x
 
 
