@@ -565,6 +565,8 @@ def run_mine(args):
         rp = ilu._region_for(sw)
         if rp is None:
             return "tickets"
+        if rp is dv.SMALL:
+            return "small"
         return "two_stage" if rp is dv.TWO_STAGE else ("cta" if rp is dv.CTA else "region")
     impl = {sw: impl_of(sw) for sw in ("factor", "fwd", "bwd")}
 

@@ -276,6 +276,21 @@ int jv_solve_level(int which, const int32_t* row_start, const int32_t* col, cons
                    const double* in, double* out, void* stream);
 int jv_check_zero_diag(int32_t n, const double* val, const int32_t* diag_pos,
                        int32_t* row, void* stream);
+/* Small systems: one sweep in ONE thread block with the vector, the sweep's
+ * dependency entries, the diagonal and the level lists all in shared memory;
+ * levels separated by __syncthreads, thread per row, the reference chain
+ * (_kernels.py:348-366) — bitwise the other solve paths.  order: rows sorted
+ * by level of the sweep's DAG; lptr[nlev + 1]: level bounds in it;
+ * estart[n + 1]: prefix sum of the rows' dependency counts (forward: strict-
+ * lower entries, backward: strict-upper), nent = estart[n]; width: rows of
+ * the largest level (narrow levels run with fewer warps).  Fits when
+ * jv_solve_small_bytes(...) <= jv_solve_small_max().                        */
+int64_t jv_solve_small_bytes(int which, int32_t n, int32_t nlev, int64_t nent);
+int64_t jv_solve_small_max(void);
+int jv_solve_small(int which, int32_t n, const int32_t* row_start, const int32_t* col,
+                   const double* val, const int32_t* diag_pos, const int32_t* order,
+                   const int32_t* lptr, int32_t nlev, const int32_t* estart, int64_t nent,
+                   int32_t width, const double* in, double* out, void* stream);
 /* schedule builder: cut every level of a level_sort result into batches of
  * at most 32 rows (one warp; rows of a batch never depend on each other).
  * batch_ptr sized >= n/32 + nlev + 1; *nbatch_h returned (synchronises). */

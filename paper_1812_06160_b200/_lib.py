@@ -98,6 +98,9 @@ _SIGS = {
     "jv_tail_plan_free": [c_int64],
     "jv_scatter": [c_int64, _P, _P, _P, _P],
     "jv_hop_latency": [c_int32, POINTER(c_double)],
+    "jv_solve_small_bytes": [c_int, c_int32, c_int32, c_int64],
+    "jv_solve_small_max": [],
+    "jv_solve_small": [c_int, c_int32, _P, _P, _P, _P, _P, _P, c_int32, _P, c_int64, c_int32, _P, _P, _P],
     "jv_cta_max_rows": [],
     "jv_cta_plan_build": [c_int32, _P, _P, _P, c_int, _P],
     "jv_cta_plan_export": [c_int64, _P, _P, _P, _P, _P, POINTER(c_int64)],
@@ -119,6 +122,8 @@ _RESTYPES = {
     "jv_tail_plan_build": c_int64,
     "jv_cta_plan_build": c_int64,
     "jv_cta_smem": c_int64,
+    "jv_solve_small_bytes": c_int64,
+    "jv_solve_small_max": c_int64,
 }
 
 _lib = None
@@ -150,7 +155,7 @@ def exported_symbols():
 # launch_counts tallies them (bench.py reports the count it observes)
 _ONE_LAUNCH = {"jv_factor", "jv_solve", "jv_region_run", "jv_pack_values", "jv_pack_values2", "jv_row_norms",
                "jv_reset_row", "jv_spmv", "jv_spmv_rows", "jv_gather", "jv_check_zero_diag",
-               "jv_solve_level", "jv_tail_upper", "jv_scatter", "jv_cta_run"}
+               "jv_solve_level", "jv_tail_upper", "jv_scatter", "jv_cta_run", "jv_solve_small"}
 launch_counts = {}
 
 

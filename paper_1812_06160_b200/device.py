@@ -297,6 +297,9 @@ TWO_STAGE = {"two_stage": True, "nreg": 0}
 # autotune candidate of every sweep of a small matrix: one CTA walks the
 # levels with __syncthreads (csrc/cta.cu)
 CTA = {"cta": True, "nreg": 0}
+# autotune candidate of the solves of a small matrix: one thread block with
+# the whole sweep in shared memory (jv_solve_small, csrc/solve.cu)
+SMALL = {"small": True, "nreg": 0}
 _CTA_MAX = []
 
 
@@ -697,6 +700,8 @@ class DevIlu:
             cands.append(TWO_STAGE)
         if 0 < self.n <= cta_max_rows() and self.cta_ok(sweep):
             cands.append(CTA)
+        if sweep != "factor" and self._small_plan(0 if sweep == "fwd" else 1) is not None:
+            cands.append(SMALL)
         if len(cands) == 1:
             self.autotune_ms[sweep] = ()
             return None
@@ -722,6 +727,8 @@ class DevIlu:
                 self._solve_tickets(which, vin, vout)
             elif rp is CTA:
                 self._solve_cta(which, vin, vout)
+            elif rp is SMALL:
+                self._solve_small(which, vin, vout)
             else:
                 self._region_run(rp, 1 + which, vin, vout, self.sbox)
 
@@ -750,7 +757,7 @@ class DevIlu:
         best = cands[k] if times[k] < 0.97 * times[0] else None
         self.autotune_ms[sweep] = tuple(times)
         for k in [k for k, v in self._rstreams.items() if k[0] == sweep and v is not best
-                  and v is not TWO_STAGE and v is not CTA]:
+                  and v is not TWO_STAGE and v is not CTA and v is not SMALL]:
             del self._rstreams[k]   # free the losing plans
         return best
 
@@ -1147,6 +1154,45 @@ class DevIlu:
     def _solve_cta(self, which, b, out):
         self._cta_run("fwd" if which == 0 else "bwd", b, out)
 
+    # small systems: one sweep in one thread block, all in shared memory ---
+    def _level_lists(self, which):
+        """(rows in level order (device int32), level bounds (numpy), depth)
+        of one sweep's DAG, from its schedule."""
+        sched = self.fwd_schedule() if which == 0 else self.bwd_schedule()
+        nclass = len(sched.steps) if hasattr(sched, "steps") else 2
+        order = sched.order
+        lev = (sched.keys[order.long()] // nclass).cpu().numpy()
+        nlev = int(lev.max()) + 1 if lev.size else 0
+        return order, np.searchsorted(lev, np.arange(nlev + 1)), nlev
+
+    def _small_plan(self, which):
+        """Arguments of jv_solve_small for one direction, or None when the
+        sweep does not fit one thread block's shared memory (cached)."""
+        cache = self.__dict__.setdefault("_small", {})
+        if which not in cache:
+            t = torch()
+            lib = _lib.load()
+            plan = None
+            if 0 < self.n <= (1 << 15):
+                n = self.n
+                rs, dg = self.row_start[:n + 1].long(), self.diag_pos[:n].long()
+                cnt = (dg - rs[:n]) if which == 0 else (rs[1:] - dg - 1)
+                nent = int(cnt.sum().item())
+                order, lptr, nlev = self._level_lists(which)
+                if lib.jv_solve_small_bytes(which, n, nlev, nent) <= lib.jv_solve_small_max():
+                    estart = t.zeros(n + 1, dtype=t.int32, device="cuda")
+                    estart[1:] = t.cumsum(cnt, 0).to(t.int32)
+                    width = int(np.diff(lptr).max()) if nlev else 0
+                    plan = (order.contiguous(), i32(lptr), nlev, estart, nent, width)
+            cache[which] = plan
+        return cache[which]
+
+    def _solve_small(self, which, b, out):
+        order, lptr, nlev, estart, nent, width = self._small_plan(which)
+        _lib.call("jv_solve_small", which, self.n, ptr(self.row_start), ptr(self.col), ptr(self.val),
+                  ptr(self.diag_pos), ptr(order), ptr(lptr), nlev, ptr(estart), nent, width, ptr(b),
+                  ptr(out), stream())
+
     # streamed drop-in factorization: host values in, factors out -------
     STREAM_CHUNKS = 8
 
@@ -1254,6 +1300,9 @@ class DevIlu:
         if rp is CTA:
             self._solve_cta(which, b, out)
             return out
+        if rp is SMALL:
+            self._solve_small(which, b, out)
+            return out
         if rp is not None:
             # the backward sweep's value pack depends only on the factors:
             # refresh it on a side stream while the forward region kernel
@@ -1269,7 +1318,7 @@ class DevIlu:
                        else self.region_stream("bwd"))
             ev = []
             hook = None
-            if nxt is not None and nxt["pver"] != self._vver:
+            if nxt is not None and "pver" in nxt and nxt["pver"] != self._vver:   # (a region plan)
                 hook = lambda: ev.append(self._side_pack(nxt))
             self._region_run(rp, 1 + which, b, out, self.sbox, hook)
             if ev:
