@@ -385,7 +385,7 @@ namespace {
 constexpr int kSmallThreads = 1024;
 
 struct SmallArgs {
-  int which, n, nlev, nent, active;
+  int which, n, nlev, nent, active, width;
   const int32_t* rs;
   const int32_t* col;
   const double* val;
@@ -451,6 +451,63 @@ __global__ void __launch_bounds__(kSmallThreads, 1) solve_small_kernel(SmallArgs
   // over 2 warps is much cheaper than over 32; exited threads do not count)
   const int nt = A.active;
   if (tid >= nt) return;
+  if (A.width <= nt) {
+    // One row per thread and level: everything a row needs except the x
+    // values it depends on is independent of the sweep, so it is fetched
+    // through a register pipeline three levels deep (level bounds -> row ->
+    // entry range and diagonal -> first four entries); each shared-memory
+    // load is consumed an iteration after it was issued, and only
+    // x[col] -> chain -> store -> barrier stays on the per-level path.
+    const int nlev = A.nlev;
+    auto bounds_of = [&](int L) { return L < nlev ? make_int2(sl[L] + tid, sl[L + 1]) : make_int2(0, 0); };
+    auto row_of = [&](int2 b) { return b.x < b.y ? so[b.x] : -1; };
+    struct Row { int r, e0, cnt; double d, xin; };
+    auto range_of = [&](int r) {
+      Row o{r, 0, 0, 1.0, 0.0};
+      if (r >= 0) {
+        o.e0 = se[r];
+        o.cnt = se[r + 1] - o.e0;
+        o.xin = x[r];                       // still the right-hand side: only its owner writes it
+        if (A.which) o.d = sd[r];
+      }
+      return o;
+    };
+    Row C = range_of(row_of(bounds_of(0)));
+    Row B = range_of(row_of(bounds_of(1)));
+    int rA = row_of(bounds_of(2));
+    int2 bn = bounds_of(3);
+    double cv[4];
+    int cc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      cv[k] = k < C.cnt ? sv[C.e0 + k] : 0.0;
+      cc[k] = k < C.cnt ? sc[C.e0 + k] : 0;
+    }
+    for (int L = 0; L < nlev; ++L) {
+      if (C.r >= 0) {
+        double s = C.xin;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < C.cnt) s = jv::dsub(s, jv::dmul(cv[k], x[cc[k]]));
+        for (int e = C.e0 + 4; e < C.e0 + C.cnt; ++e) s = jv::dsub(s, jv::dmul(sv[e], x[sc[e]]));
+        if (A.which) s = jv::ddiv(s, C.d);
+        x[C.r] = s;
+      }
+      // advance the pipeline (none of these loads is used before the next iteration)
+      C = B;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cv[k] = k < C.cnt ? sv[C.e0 + k] : 0.0;
+        cc[k] = k < C.cnt ? sc[C.e0 + k] : 0;
+      }
+      B = range_of(rA);
+      rA = row_of(bn);
+      bn = bounds_of(L + 4);
+      __syncthreads();
+    }
+    for (int r = tid; r < n; r += nt) A.out[r] = x[r];
+    return;
+  }
   for (int L = 0; L < A.nlev; ++L) {
     const int hi = sl[L + 1];
     for (int i = sl[L] + tid; i < hi; i += nt) {
@@ -501,8 +558,8 @@ extern "C" int jv_solve_small(int which, int32_t n, const int32_t* row_start, co
   }();
   (void)once;
   const int active = min(kSmallThreads, max(64, (width + 31) / 32 * 32));
-  SmallArgs A{which, n, nlev, (int)nent, active, row_start, col, val, diag_pos, order, lptr, estart,
-              in, out};
+  SmallArgs A{which, n, nlev, (int)nent, active, width, row_start, col, val, diag_pos, order, lptr,
+              estart, in, out};
   solve_small_kernel<<<1, kSmallThreads, bytes, (cudaStream_t)stream>>>(A);
   JV_CHECK_LAUNCH("jv_solve_small");
   return JV_OK;
